@@ -1,0 +1,238 @@
+/*
+ * mpir_gpu.h -- C-ABI of the B200 mixed-precision iterative-refinement (IR)
+ * hot path: interprecision copy, low-precision LU with partial pivoting,
+ * triangular solves, and the TR-precision residual.
+ *
+ * The reference (proj/ in arxiv/paper_2311_14616, "mpir") has no FFI layer of
+ * its own: its boundary is the header-only C++ API
+ *   MPFactorization<TW,TF,TR>   proj/include/mpir/mp_structures.hpp:97-213
+ *   mp_lu / mp_refactor         proj/include/mpir/mp_structures.hpp:215-237
+ *   ir_solve_report / ir_solve  proj/include/mpir/ir_engine.hpp:291-304
+ *   residual_tr                 proj/include/mpir/ir_engine.hpp:277-287
+ * plus the kernels it is built from (dense_lu.hpp, matrix.hpp). Every entry
+ * point below names the reference function it replaces. The C++ twin of the
+ * reference API (mpir_gpu.hpp) and the Python mirror of the reference module
+ * (paper_2311_14616_b200/mpir.py) are thin layers over these symbols.
+ *
+ * Conventions
+ *  - Matrices are n x n, column-major, leading dimension n (matrix.hpp:17-61).
+ *  - Precision codes follow mpir::Precision (precision.hpp:20-25).
+ *    B16 data is IEEE binary16 stored as uint16_t bits (half.hpp:25-192).
+ *  - Every call returns an int status (MPIRG_OK or an MPIRG_ERR_* code that
+ *    names the reference exception type, errors.hpp:14-94) and, when err is
+ *    non-NULL, fills err with the exception payload.
+ *  - Calls are synchronous, like the reference API. Kernel-level entry points
+ *    take device pointers and a cudaStream_t passed as void* (NULL = the
+ *    legacy default stream); they synchronise that stream before returning.
+ *  - No torch types cross this boundary; there is no CPU fallback. A missing
+ *    or unusable GPU yields MPIRG_ERR_CUDA.
+ */
+#ifndef MPIR_GPU_H
+#define MPIR_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPIRG_ABI_VERSION 1
+
+/* mpir::Precision, precision.hpp:20-25 */
+enum mpirg_precision { MPIRG_B64 = 0, MPIRG_B32 = 1, MPIRG_B16 = 2 };
+
+/* Status codes; one per reference exception type (errors.hpp:14-94). */
+enum mpirg_status {
+  MPIRG_OK = 0,
+  MPIRG_ERR_OVERFLOW = 1,       /* OverflowDetected   (precision.hpp:177-180) */
+  MPIRG_ERR_SINGULAR = 2,       /* SingularPivot{column} (dense_lu.hpp:76-77) */
+  MPIRG_ERR_NONFINITE = 3,      /* NonFiniteResult{rhist,dhist} (ir_engine.hpp:217-231) */
+  MPIRG_ERR_DIMENSION = 4,      /* DimensionMismatch */
+  MPIRG_ERR_INVALID_CONFIG = 5, /* InvalidConfig      (precision.hpp:222-230) */
+  MPIRG_ERR_INVALID_PARAM = 6,  /* InvalidParameter   (ir_engine.hpp:29-47) */
+  MPIRG_ERR_INVALID_SIZE = 7,   /* InvalidSize        (matrix.hpp:24-28) */
+  MPIRG_ERR_CUDA = 8,           /* CUDA runtime failure (no reference analogue) */
+  MPIRG_ERR_NCCL = 9            /* NCCL failure (no reference analogue) */
+};
+
+/* mpir::StopReason, ir_engine.hpp:66-90 */
+enum mpirg_stop_reason {
+  MPIRG_SMALL_RESIDUAL = 0,
+  MPIRG_SMALL_BACKWARD_ERROR = 1,
+  MPIRG_RESIDUAL_STAGNATION = 2,
+  MPIRG_CORRECTION_STAGNATION = 3,
+  MPIRG_ITERATION_LIMIT = 4
+};
+
+/* LU arithmetic mode. EXACT reproduces lu_inplace (dense_lu.hpp:50-109)
+ * bit for bit for every factor precision. TC is the fp16 tensor-core
+ * trailing update (tcgen05, fp32 accumulation in TMEM, one rounding to fp16
+ * per panel block); it is only valid for TF = B16 and is tolerance-checked,
+ * not bitwise. */
+enum mpirg_lu_mode { MPIRG_LU_EXACT = 0, MPIRG_LU_TC = 1 };
+
+/* Exception payload. */
+typedef struct mpirg_error {
+  int status;        /* same as the return value */
+  int column;        /* SingularPivot::column; -1 otherwise */
+  double value;      /* OverflowDetected: the first offending value */
+  char message[256]; /* the reference's what() text where it has one */
+} mpirg_error;
+
+/* PrecisionConfig (precision.hpp:210-231) + FactorOptions
+ * (mp_structures.hpp:82-90) + device/tuning knobs. */
+typedef struct mpirg_config {
+  int tw;         /* working precision (B64 or B32) */
+  int tf;         /* factorization precision */
+  int tr;         /* residual precision */
+  int on_the_fly; /* -1: resolve like mp_structures.hpp:118-121; 0/1 explicit */
+  int resid_term; /* FactorOptions::resid_term (default 1) */
+  int lu_mode;    /* enum mpirg_lu_mode (default EXACT) */
+  int nb;         /* LU panel width; 0 = automatic */
+  int device;     /* CUDA device ordinal; -1 = current device */
+} mpirg_config;
+
+/* TermParams, ir_engine.hpp:29-47 (defaults cr=1, ce=1, rmax=0.5, litmax=10). */
+typedef struct mpirg_term_params {
+  double cr;
+  double ce;
+  double rmax;
+  int litmax;
+} mpirg_term_params;
+
+/* SolveReport<TW>, ir_engine.hpp:96-105. The caller owns every buffer:
+ * sol holds n values of TW (host or device memory per sol_on_device);
+ * rhist/dhist hold hist_capacity doubles (capacity >= litmax suffices).
+ * On MPIRG_ERR_NONFINITE the partial histories are written, like the
+ * NonFiniteResult payload. */
+typedef struct mpirg_report {
+  void *sol;
+  int sol_on_device;
+  double *rhist;
+  double *dhist;
+  int hist_capacity;
+  int rhist_len;
+  int dhist_len;
+  int reason;          /* enum mpirg_stop_reason */
+  double solve_ms;     /* device time of the IR loop (CUDA events) */
+} mpirg_report;
+
+typedef struct mpirg_factorization mpirg_factorization;
+
+/* ---------------------------------------------------------------------------
+ * Library / config
+ * ------------------------------------------------------------------------- */
+int mpirg_abi_version(void);
+/* Number of CUDA devices visible; 0 when no GPU (then every GPU call fails). */
+int mpirg_device_count(void);
+/* resolve_config (mp_structures.hpp:44-59): fills TF/TR/on_the_fly defaults.
+ * Pass tf/tr/on_the_fly = -1 for "not given". */
+int mpirg_resolve_config(int tw, int tf, int tr, int on_the_fly, mpirg_config *out,
+                         mpirg_error *err);
+/* update_parms (ir_engine.hpp:49-64). NaN in a field = "not given"; litmax<=0 not given. */
+int mpirg_update_parms(double cr, double ce, double rmax, int litmax,
+                       mpirg_term_params *out, mpirg_error *err);
+double mpirg_machine_eps(int precision);   /* precision.hpp:43-54 */
+double mpirg_unit_roundoff(int precision); /* precision.hpp:28-39 */
+
+/* ---------------------------------------------------------------------------
+ * MPFactorization<TW,TF,TR> (mp_structures.hpp:97-213)
+ * ------------------------------------------------------------------------- */
+/* Constructor: takes a copy of the TW matrix a (host or device memory), then
+ * refactor(): one-norm of a_high in TW, demotion into the factor storage with
+ * overflow/underflow checks, LU in place. */
+int mpirg_factorization_create(mpirg_factorization **out, int n, const mpirg_config *cfg,
+                               const void *a, int a_on_device, mpirg_error *err);
+/* refactor(const Matrix<TW>&) (mp_structures.hpp:155-169). a == NULL
+ * refactors the resident a_high (the reference's self-refactor, no copy).
+ * Every device buffer is reused; pointers stay stable. */
+int mpirg_factorization_refactor(mpirg_factorization *f, const void *a, int a_on_device,
+                                 mpirg_error *err);
+void mpirg_factorization_destroy(mpirg_factorization *f);
+
+int mpirg_factorization_n(const mpirg_factorization *f);
+int mpirg_factorization_config(const mpirg_factorization *f, mpirg_config *out);
+double mpirg_factorization_a_norm1(const mpirg_factorization *f);
+int mpirg_factorization_demotion_underflowed(const mpirg_factorization *f);
+size_t mpirg_factorization_matrix_bytes(const mpirg_factorization *f);
+/* Device time (ms) of the last refactor: one-norm + demotion + LU. */
+double mpirg_factorization_last_factor_ms(const mpirg_factorization *f);
+/* Host copies of the factor state (lazy device->host mirrors). */
+int mpirg_factorization_get_ipiv(const mpirg_factorization *f, int *ipiv);
+int mpirg_factorization_get_pivots(const mpirg_factorization *f, int *perm);
+int mpirg_factorization_get_packed_lu(const mpirg_factorization *f, void *out_tf);
+int mpirg_factorization_get_a_high(const mpirg_factorization *f, void *out_tw);
+/* Stable device pointers (column-major n x n). */
+const void *mpirg_factorization_a_high_device(const mpirg_factorization *f);
+const void *mpirg_factorization_packed_lu_device(const mpirg_factorization *f);
+const int *mpirg_factorization_ipiv_device(const mpirg_factorization *f);
+/* The CUDA stream every call on this handle runs on (cudaStream_t). */
+void *mpirg_factorization_stream(const mpirg_factorization *f);
+
+/* ir_solve_report(f, b, tp) (ir_engine.hpp:291-297, loop 186-271). b holds n
+ * values of TW. tp == NULL uses the defaults. */
+int mpirg_ir_solve(mpirg_factorization *f, const void *b, int b_on_device,
+                   const mpirg_term_params *tp, mpirg_report *rep, mpirg_error *err);
+/* residual_tr(f, x, b) (ir_engine.hpp:277-287): r (n values of TR) = b - A x,
+ * x and b in TW. Host or device buffers per on_device. */
+int mpirg_residual_tr(mpirg_factorization *f, const void *x, const void *b, void *r,
+                      int on_device, mpirg_error *err);
+
+/* ---------------------------------------------------------------------------
+ * Kernel-level entry points (device pointers, explicit stream)
+ * ------------------------------------------------------------------------- */
+/* demote_matrix_into<To,From> (matrix.hpp:74-85) with demote_checked
+ * (precision.hpp:172-185). Overflow is reported for the first offending
+ * element in storage order; *underflow (optional) receives the sticky flag. */
+int mpirg_demote(int from, int to, size_t count, const void *src, void *dst, int *underflow,
+                 void *stream, mpirg_error *err);
+/* matrix_one_norm<T> (mp_structures.hpp:22-36), accumulated in T. */
+int mpirg_one_norm(int prec, int rows, int cols, const void *a, double *out, void *stream,
+                   mpirg_error *err);
+/* lu_factor / lu_factor_half (dense_lu.hpp:151-171): in-place LU of the
+ * n x n matrix a (precision prec), ipiv[n] (device) receives the swap rows. */
+int mpirg_lu_factor(int prec, int n, void *a, int *ipiv, int lu_mode, int nb, void *stream,
+                    mpirg_error *err);
+/* solve_mps_into<TS,TF> (dense_lu.hpp:175-182): in place on x (TS). */
+int mpirg_solve_mps(int ts, int tf, int n, const void *packed, const int *ipiv, void *x,
+                    void *stream, mpirg_error *err);
+/* solve_lps_into<TW,TF> (dense_lu.hpp:204-232): in place on r_to_d (TW),
+ * scratch holds n values of TF. */
+int mpirg_solve_lps(int tw, int tf, int n, const void *packed, const int *ipiv, void *r_to_d,
+                    void *scratch, int *underflow, void *stream, mpirg_error *err);
+/* detail::residual_into<TW,TR> (ir_engine.hpp:115-139): r = b - A x in TR,
+ * compensated; a, b in TW; x, r in TR. */
+int mpirg_residual(int tw, int tr, int n, const void *a, const void *x, const void *b,
+                   void *r, void *stream, mpirg_error *err);
+
+/* ---------------------------------------------------------------------------
+ * Batched independent systems (BASELINE config 5b): count systems of size n,
+ * each a separate MPFactorization<TW,TF,TR> + ir_solve_report with the same
+ * termination parameters. a: count*n*n TW (system s at offset s*n*n);
+ * b, sol: count*n TW. rhist/dhist: count*hist_capacity; lens/reasons: count.
+ * Per-system errors are reported in status[count] (0 = ok) and the call
+ * returns the first non-OK status.
+ * ------------------------------------------------------------------------- */
+int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *a,
+                         const void *b, int on_device, const mpirg_term_params *tp,
+                         void *sol, double *rhist, double *dhist, int hist_capacity,
+                         int *rhist_len, int *reason, int *status, double *device_ms,
+                         mpirg_error *err);
+
+/* ---------------------------------------------------------------------------
+ * Seeded input generators (host; not on the timed path). See problems.cpp.
+ * ------------------------------------------------------------------------- */
+void mpirg_gen_uniform_matrix(int rows, int cols, uint64_t seed, double lo, double hi,
+                              double *out);
+void mpirg_gen_normal_matrix(int rows, int cols, uint64_t seed, double *out);
+void mpirg_gen_diag_dominant(int n, uint64_t seed, double shift, double *out);
+void mpirg_gen_greens_operator(int n, double alpha, double *out);
+void mpirg_gen_integral_rhs(int n, double alpha, double *out);
+void mpirg_gen_matvec_compensated_f64(int n, const double *a, const double *x, double *y);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPIR_GPU_H */

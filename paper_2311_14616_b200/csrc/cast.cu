@@ -1,0 +1,262 @@
+// K1 -- interprecision copy A_F = I_W^F(A) and the refactor one-norm.
+//
+// Replaces, bit for bit:
+//   demote_matrix_into<To,From>   proj/include/mpir/matrix.hpp:74-85
+//   demote_checked<To>            proj/include/mpir/precision.hpp:172-185
+//   matrix_one_norm<T>            proj/include/mpir/mp_structures.hpp:22-36
+// Demotion is RNE (static_cast / F16C / single-rounding double->half). An
+// element whose |x| exceeds the target's largest finite value raises
+// OverflowDetected in the reference at the first such element in storage
+// order; here every offender does an atomicMin on its storage index so the
+// host reports the same one. Underflow (x != 0 rounds to 0) is sticky.
+// The one-norm is a sequential per-column sum in the matrix's own precision
+// (one lane per column, rows in order), max over columns ignoring NaN like
+// std::max(best, s).
+#include <cfloat>
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mpirg
+{
+
+namespace
+{
+
+__device__ __forceinline__ double max_finite_of(int p)
+{
+  return p == B64 ? DBL_MAX : (p == B32 ? (double)FLT_MAX : 65504.0);
+}
+
+template <typename From, typename To>
+__device__ __forceinline__ To demote_one(From x, size_t idx, double maxf, bool &uf,
+                                         unsigned long long &ovf)
+{
+  const double xd = to_d(x);
+  if (isfinite(xd) && fabs(xd) > maxf && idx < ovf)
+    ovf = idx;
+  const To y = demote<To, From>(x);
+  if (to_d(y) == 0.0 && xd != 0.0)
+    uf = true;
+  return y;
+}
+
+__device__ __forceinline__ void flush_flags(bool uf, unsigned long long ovf, DevInfo *info)
+{
+  const unsigned m = __activemask();
+  if (__any_sync(m, uf) && (threadIdx.x & 31) == (__ffs(m) - 1))
+    info->underflow = 1;
+  if (ovf != ~0ull)
+    atomicMin(&info->overflow_index, ovf);
+}
+
+// Elementwise demotion, 8 elements per thread per iteration.
+template <typename From, typename To>
+__global__ void demote_kernel(const From *__restrict__ src, To *__restrict__ dst, size_t count,
+                              DevInfo *info)
+{
+  const double maxf = max_finite_of(std::is_same<To, double>::value
+                                        ? B64
+                                        : (std::is_same<To, float>::value ? B32 : B16));
+  bool uf = false;
+  unsigned long long ovf = ~0ull;
+  const size_t nvec = count / 8;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < nvec; v += stride)
+  {
+    From in[8];
+    To out[8];
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src + v * 8);
+#pragma unroll
+    for (int q = 0; q < (int)(8 * sizeof(From) / 16); ++q)
+      reinterpret_cast<uint4 *>(in)[q] = __ldcs(s4 + q);
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      out[e] = demote_one<From, To>(in[e], v * 8 + e, maxf, uf, ovf);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst + v * 8);
+#pragma unroll
+    for (int q = 0; q < (int)(8 * sizeof(To) / 16); ++q)
+      d4[q] = reinterpret_cast<const uint4 *>(out)[q];
+  }
+  for (size_t i = nvec * 8 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += stride)
+    dst[i] = demote_one<From, To>(src[i], i, maxf, uf, ovf);
+  flush_flags(uf, ovf, info);
+}
+
+template <typename T> __device__ __forceinline__ T ldcs_t(const T *p) { return __ldcs(p); }
+template <> __device__ __forceinline__ h16 ldcs_t<h16>(const h16 *p)
+{
+  return h16{__ldcs(reinterpret_cast<const unsigned short *>(p))};
+}
+
+// Plain |x| in T arithmetic and the T-typed running sum.
+__device__ __forceinline__ double absv(double v) { return fabs(v); }
+__device__ __forceinline__ float absv(float v) { return fabsf(v); }
+__device__ __forceinline__ h16 absv(h16 v) { return h16{(uint16_t)(v.bits & 0x7fffu)}; }
+__device__ __forceinline__ double acc_add(double s, double v) { return __dadd_rn(s, v); }
+__device__ __forceinline__ float acc_add(float s, float v) { return __fadd_rn(s, v); }
+__device__ __forceinline__ h16 acc_add(h16 s, h16 v) { return hadd(s, v); }
+
+// Fused cast + one-norm. One warp owns a stripe of 32 columns and walks down
+// the rows in 32x32 tiles: lane = row for the coalesced load/demote/store,
+// then lane = column for the in-order column sum through a padded smem tile.
+// To == From (TF == TW) is a plain copy. NORM_ONLY skips the store.
+template <typename From, typename To, bool NORM_ONLY>
+__global__ void __launch_bounds__(128) cast_norm_kernel(const From *__restrict__ src,
+                                                        To *__restrict__ dst, int rows,
+                                                        int cols,
+                                                        unsigned long long *norm_bits,
+                                                        DevInfo *info)
+{
+  __shared__ From tile[4][32][33];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int c0 = (blockIdx.x * 4 + w) * 32;
+  if (c0 >= cols)
+    return;
+  const int ncol = min(32, cols - c0);
+  const double maxf =
+      NORM_ONLY ? 0.0
+                : max_finite_of(std::is_same<To, double>::value
+                                    ? B64
+                                    : (std::is_same<To, float>::value ? B32 : B16));
+  bool uf = false;
+  unsigned long long ovf = ~0ull;
+  From sum = From{};
+  if constexpr (std::is_same<From, h16>::value)
+    sum = h16{0};
+  else
+    sum = From(0);
+
+  From cur[32], nxt[32];
+  auto load_tile = [&](int r0, From *v) {
+    const int r = r0 + lane;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+    {
+      if (c < ncol && r < rows)
+        v[c] = ldcs_t(src + (size_t)(c0 + c) * rows + r);
+      else
+        v[c] = From{};
+    }
+  };
+  load_tile(0, cur);
+  for (int r0 = 0; r0 < rows; r0 += 32)
+  {
+    if (r0 + 32 < rows)
+      load_tile(r0 + 32, nxt);
+    const int r = r0 + lane;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+    {
+      if (c < ncol && r < rows)
+      {
+        if constexpr (!NORM_ONLY)
+        {
+          const size_t idx = (size_t)(c0 + c) * rows + r;
+          dst[idx] = demote_one<From, To>(cur[c], idx, maxf, uf, ovf);
+        }
+        tile[w][c][lane] = absv(cur[c]);
+      }
+    }
+    __syncwarp();
+    const int nr = min(32, rows - r0);
+    if (lane < ncol)
+    {
+      for (int i = 0; i < nr; ++i)
+        sum = acc_add(sum, tile[w][lane][i]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      cur[c] = nxt[c];
+  }
+  // best = std::max(best, double(s)): NaN sums never win; sums are >= 0.
+  const double sd = lane < ncol ? to_d(sum) : 0.0;
+  unsigned long long bits = isnan(sd) ? 0ull : abs_bits(sd);
+  bits = warp_max_u64(bits);
+  if (lane == 0)
+    atomicMax(norm_bits, bits);
+  if constexpr (!NORM_ONLY)
+    flush_flags(uf, ovf, info);
+}
+
+template <typename From, typename To>
+void demote_t(const void *src, void *dst, size_t count, DevInfo *info, cudaStream_t s)
+{
+  if (count == 0)
+    return;
+  const size_t nvec = (count + 7) / 8;
+  int grid = (int)std::min<size_t>((nvec + 255) / 256, 148 * 8);
+  if (grid < 1)
+    grid = 1;
+  demote_kernel<From, To><<<grid, 256, 0, s>>>(static_cast<const From *>(src),
+                                              static_cast<To *>(dst), count, info);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+template <typename From, typename To, bool NORM_ONLY>
+void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long long *nb,
+                 DevInfo *info, cudaStream_t s)
+{
+  if (rows <= 0 || cols <= 0)
+    return;
+  const int stripes = (cols + 31) / 32;
+  const int grid = (stripes + 3) / 4;
+  cast_norm_kernel<From, To, NORM_ONLY><<<grid, 128, 0, s>>>(
+      static_cast<const From *>(src), static_cast<To *>(dst), rows, cols, nb, info);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace
+
+void launch_demote(int from, int to, const void *src, void *dst, size_t count, DevInfo *info,
+                   cudaStream_t s)
+{
+  if (from == B64 && to == B64)
+    demote_t<double, double>(src, dst, count, info, s);
+  else if (from == B64 && to == B32)
+    demote_t<double, float>(src, dst, count, info, s);
+  else if (from == B64 && to == B16)
+    demote_t<double, h16>(src, dst, count, info, s);
+  else if (from == B32 && to == B32)
+    demote_t<float, float>(src, dst, count, info, s);
+  else if (from == B32 && to == B16)
+    demote_t<float, h16>(src, dst, count, info, s);
+  else if (from == B16 && to == B16)
+    demote_t<h16, h16>(src, dst, count, info, s);
+  else
+    throw std::invalid_argument("demotion must not gain precision");
+}
+
+void launch_cast_norm(int from, int to, int rows, int cols, const void *src, void *dst,
+                      unsigned long long *nb, DevInfo *info, cudaStream_t s)
+{
+  if (from == B64 && to == B64)
+    cast_norm_t<double, double, false>(rows, cols, src, dst, nb, info, s);
+  else if (from == B64 && to == B32)
+    cast_norm_t<double, float, false>(rows, cols, src, dst, nb, info, s);
+  else if (from == B64 && to == B16)
+    cast_norm_t<double, h16, false>(rows, cols, src, dst, nb, info, s);
+  else if (from == B32 && to == B32)
+    cast_norm_t<float, float, false>(rows, cols, src, dst, nb, info, s);
+  else if (from == B32 && to == B16)
+    cast_norm_t<float, h16, false>(rows, cols, src, dst, nb, info, s);
+  else
+    throw std::invalid_argument("unsupported cast");
+}
+
+void launch_one_norm(int prec, int rows, int cols, const void *src, unsigned long long *nb,
+                     cudaStream_t s)
+{
+  if (prec == B64)
+    cast_norm_t<double, double, true>(rows, cols, src, nullptr, nb, nullptr, s);
+  else if (prec == B32)
+    cast_norm_t<float, float, true>(rows, cols, src, nullptr, nb, nullptr, s);
+  else
+    cast_norm_t<h16, h16, true>(rows, cols, src, nullptr, nb, nullptr, s);
+}
+
+}  // namespace mpirg

@@ -1,0 +1,112 @@
+// Launcher declarations for the IR hot-path kernels (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+
+namespace mpirg
+{
+
+struct CudaError : std::runtime_error
+{
+  cudaError_t code;
+  CudaError(cudaError_t c, const char *expr, const char *file, int line)
+    : std::runtime_error(std::string(cudaGetErrorString(c)) + " in " + expr + " at " + file +
+                         ":" + std::to_string(line)),
+      code(c)
+  {
+  }
+};
+
+// ---- K1: interprecision copy --------------------------------------------
+// Elementwise demotion (matrix.hpp:74-85 + precision.hpp:172-185), any length.
+void launch_demote(int from, int to, const void *src, void *dst, size_t count, DevInfo *info,
+                   cudaStream_t s);
+// Fused refactor prologue (mp_structures.hpp:161-163): one read of the TW
+// matrix produces the TF copy, the column-sum one-norm in TW (bits of the
+// double max in *norm_bits, which must be zeroed) and the demotion flags.
+void launch_cast_norm(int from, int to, int rows, int cols, const void *src, void *dst,
+                      unsigned long long *norm_bits, DevInfo *info, cudaStream_t s);
+void launch_one_norm(int prec, int rows, int cols, const void *src,
+                     unsigned long long *norm_bits, cudaStream_t s);
+
+// ---- K2-K5: blocked right-looking LU with partial pivoting --------------
+struct LuWorkspace
+{
+  int n = 0;
+  int nb = 0;
+  int npanels = 0;
+  int2 *moves = nullptr;  // [npanels][2*nb] (dst,src) row moves of each panel
+  int *nmoves = nullptr;  // [npanels]
+};
+// Chooses the panel width for n and the factor precision (0 = auto).
+int lu_choose_nb(int prec, int n, int requested);
+void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb);
+void lu_workspace_free(LuWorkspace &ws);
+// In-place LU of the n x n column-major matrix a (precision prec). ipiv[k]
+// receives the pivot row of step k (dense_lu.hpp:79); perm (optional) the
+// accumulated permutation (row i of PA is row perm[i] of A). The first
+// exactly-zero pivot column is recorded in info->singular_col.
+void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWorkspace &ws,
+               DevInfo *info, cudaStream_t s);
+// perm from ipiv for callers that only hold ipiv (standalone solves).
+void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s);
+
+// ---- K6: triangular solves ------------------------------------------------
+struct TrsvWorkspace
+{
+  int n = 0;
+  int nblk = 0;
+  int *flags = nullptr;    // [2][nblk] ready flags (lower, upper), epoch-tagged
+  int *tickets = nullptr;  // [2] block tickets
+  int epoch = 0;
+};
+void trsv_workspace_alloc(TrsvWorkspace &ws, int n);
+void trsv_workspace_free(TrsvWorkspace &ws);
+
+// Substitution request. The solve runs in TS with TF factors.
+//  prologue: y_i = LPS ? TS( rin[perm[i]] / rho ) : TS( rin[perm[i]] )  (rin in TIN)
+//  epilogue (IR): d_i = LPS ? TR(y_i) * rho : TR(y_i); x_i += d_i; norms
+//  epilogue (standalone): out_i = LPS ? TIN(y_i) * rho : y_i
+struct TrsvArgs
+{
+  int ts, tf, tin;     // precisions
+  int lps;             // scaled (solve_lps_into) vs promoting (solve_mps_into)
+  int ir;              // fused refinement epilogue
+  int n;
+  const void *lu;      // packed factors (TF)
+  const int *perm;     // accumulated permutation
+  const void *rin;     // right-hand side / residual (TIN)
+  const unsigned long long *rho_bits;  // LPS scale (bits of a non-negative double), or null
+  void *y;             // scratch, n values of TS
+  void *out;           // standalone: result (TIN for LPS, TS for MPS); IR: x accumulator (TIN=TR)
+  unsigned long long *dnorm_bits;  // IR: ||d||_inf
+  unsigned long long *xnorm_bits;  // IR: ||x||_inf after the update
+  DevInfo *info;
+};
+void launch_trsv(const TrsvArgs &a, TrsvWorkspace &ws, cudaStream_t s);
+
+// ---- K7: compensated residual r = b - A x in TR -------------------------
+struct ResidualPlan
+{
+  void *tmap = nullptr;  // host copy of the CUtensorMap (128 B), owned
+  int n = 0, tw = 0;
+  const void *a = nullptr;
+};
+void residual_plan_make(ResidualPlan &p, int tw, int n, const void *a);
+void residual_plan_free(ResidualPlan &p);
+void launch_residual(const ResidualPlan &p, int tr, const void *x, const void *b, void *r,
+                     unsigned long long *rnorm_bits, cudaStream_t s);
+
+// ---- small vector kernels -------------------------------------------------
+// r = TR(b); x = 0; *bnorm_bits = ||r||_inf (refine_loop start, ir_engine.hpp:190-205)
+void launch_ir_init(int tw, int tr, int n, const void *b, void *r, void *x,
+                    unsigned long long *bnorm_bits, cudaStream_t s);
+// sol = TW(x) (ir_engine.hpp:267-269)
+void launch_ir_finish(int tw, int tr, int n, const void *x, void *sol, cudaStream_t s);
+
+}  // namespace mpirg

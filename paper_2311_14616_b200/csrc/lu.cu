@@ -1,0 +1,693 @@
+// K2-K5 -- blocked right-looking LU with partial pivoting, bitwise equal to
+// detail::lu_inplace (proj/include/mpir/dense_lu.hpp:50-109).
+//
+// Why blocking keeps the reference's bits: lu_inplace updates every element
+// a_ij once per elimination step k, in ascending k, with one rounding per
+// update (an FMA for fp32/fp64 under the reference build; r16(c - r16(l*u))
+// for binary16). A right-looking blocked LU performs exactly the same
+// per-element sequence as long as (1) the panel applies its rank-1 updates in
+// k order, (2) U12 = L11^{-1} A12 is a forward substitution in k order, and
+// (3) the trailing GEMM initialises its accumulator from A22 and walks k in
+// order with one FMA per term. Row swaps only move data, so deferring them to
+// a gather per panel changes nothing. Pivot choice is the reference's: the
+// first row (lowest index) maximising |a_ik| as a double, NaN never chosen,
+// and a NaN on the diagonal keeps p = k (dense_lu.hpp:65-78).
+//
+// Kernels per panel step (panel width nb, rows m = n - k0):
+//   lu_panel_kernel      one thread-block cluster (<= 16 CTAs, DSMEM) holds the
+//                        m x nb panel in shared memory; per column: local
+//                        argmax (warp shuffles), candidate rows broadcast into
+//                        every CTA's shared memory, one cluster barrier,
+//                        swap, scale (true division), rank-1 update.
+//                        Emits ipiv and the panel's row-move list.
+//   lu_apply_moves_kernel  applies the row moves (a permutation of <= 2nb rows)
+//                        as a gather to every column outside the panel and
+//                        to the accumulated permutation perm.
+//   lu_trsm_kernel       U12 = L11^{-1} A12, one thread per trailing column.
+//   lu_gemm_kernel       A22 -= L21 U12, SIMT register-tiled (fp32/fp64 FMA;
+//                        no TF32: that would change the factor precision).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mpirg
+{
+
+namespace
+{
+
+constexpr int PANEL_THREADS = 256;
+constexpr int PANEL_WARPS = PANEL_THREADS / 32;
+constexpr int MAX_CLUSTER = 16;
+
+template <typename T, int NB>
+struct alignas(16) CandSlot
+{
+  T row[NB];
+  double val;
+  int idx;
+  int rowid;
+};
+
+template <typename T, int NB>
+struct alignas(16) RowKSlot
+{
+  T row[NB];
+  int rowid;
+  int nan;
+  int pad[2];
+};
+
+template <typename T, int NB>
+struct PanelShared
+{
+  CandSlot<T, NB> cand[2][MAX_CLUSTER];
+  RowKSlot<T, NB> rowk[2];
+  double redv[PANEL_WARPS];
+  int redi[PANEL_WARPS];
+};
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+template <typename T, int NB>
+__host__ __device__ constexpr size_t panel_smem_bytes(int R)
+{
+  return sizeof(PanelShared<T, NB>) + align16(sizeof(int) * (size_t)R) + sizeof(T) * (size_t)NB * R;
+}
+
+// (v1,i1) beats (v2,i2): larger |a|, ties to the lower row. Sentinel v = -1.
+__device__ __forceinline__ bool better(double v1, int i1, double v2, int i2)
+{
+  return v1 > v2 || (v1 == v2 && i1 < i2);
+}
+
+__device__ __forceinline__ bool isnan_t(double v) { return isnan(v); }
+__device__ __forceinline__ bool isnan_t(float v) { return isnan(v); }
+__device__ __forceinline__ bool isnan_t(h16 v) { return (v.bits & 0x7c00u) == 0x7c00u && (v.bits & 0x3ffu); }
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(PANEL_THREADS, 1)
+    lu_panel_kernel(T *__restrict__ A, int n, int k0, int jb, int R, int *__restrict__ ipiv,
+                    int2 *__restrict__ moves, int *__restrict__ nmoves, DevInfo *info)
+{
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto &sh = *reinterpret_cast<PanelShared<T, NB> *>(smem_raw);
+  int *rowid = reinterpret_cast<int *>(smem_raw + sizeof(PanelShared<T, NB>));
+  T *P = reinterpret_cast<T *>(smem_raw + sizeof(PanelShared<T, NB>) + align16(sizeof(int) * R));
+
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int row0 = k0 + rank * R;
+  const int mloc = max(0, min(R, n - row0));
+
+  for (int c = 0; c < jb; ++c)
+  {
+    const T *col = A + (size_t)(k0 + c) * n + row0;
+    for (int i = t; i < mloc; i += PANEL_THREADS)
+      P[c * R + i] = col[i];
+  }
+  for (int i = t; i < mloc; i += PANEL_THREADS)
+    rowid[i] = row0 + i;
+  __syncthreads();
+
+  // Thread-local candidate for column 0 (rows g >= k0: all local rows).
+  double bv = -1.0;
+  int bi = INT_MAX;
+  for (int i = t; i < mloc; i += PANEL_THREADS)
+  {
+    const double a = fabs(to_d(P[i]));
+    if (!isnan(a) && better(a, row0 + i, bv, bi))
+    {
+      bv = a;
+      bi = row0 + i;
+    }
+  }
+
+  for (int j = 0; j < jb; ++j)
+  {
+    const int k = k0 + j;
+    const int par = j & 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+    {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi))
+      {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0)
+    {
+      sh.redv[warp] = bv;
+      sh.redi[warp] = bi;
+    }
+    __syncthreads();
+    double cv = sh.redv[0];
+    int ci = sh.redi[0];
+#pragma unroll
+    for (int w = 1; w < PANEL_WARPS; ++w)
+      if (better(sh.redv[w], sh.redi[w], cv, ci))
+      {
+        cv = sh.redv[w];
+        ci = sh.redi[w];
+      }
+
+    // Broadcast this CTA's candidate row (full panel row) to every CTA.
+    const int cl = (ci != INT_MAX) ? ci - row0 : -1;
+    for (int q = t; q < CS * NB; q += PANEL_THREADS)
+    {
+      const int dst = q / NB, c = q % NB;
+      CandSlot<T, NB> *rs = cluster.map_shared_rank(&sh.cand[par][rank], dst);
+      rs->row[c] = (cl >= 0 && c < jb) ? P[c * R + cl] : T{};
+    }
+    if (t < CS)
+    {
+      CandSlot<T, NB> *rs = cluster.map_shared_rank(&sh.cand[par][rank], t);
+      rs->val = cv;
+      rs->idx = ci;
+      rs->rowid = cl >= 0 ? rowid[cl] : -1;
+    }
+    // The owner of row k broadcasts it too (the pivot row's new content).
+    const bool own_k = k >= row0 && k < row0 + mloc;
+    if (own_k)
+    {
+      const int kl = k - row0;
+      for (int q = t; q < CS * NB; q += PANEL_THREADS)
+      {
+        const int dst = q / NB, c = q % NB;
+        RowKSlot<T, NB> *rk = cluster.map_shared_rank(&sh.rowk[par], dst);
+        rk->row[c] = c < jb ? P[c * R + kl] : T{};
+      }
+      if (t < CS)
+      {
+        RowKSlot<T, NB> *rk = cluster.map_shared_rank(&sh.rowk[par], t);
+        rk->rowid = rowid[kl];
+        rk->nan = isnan_t(P[j * R + kl]) ? 1 : 0;
+      }
+    }
+    cluster.sync();
+
+    // Global decision, computed redundantly by every thread.
+    double gv = -1.0;
+    int gi = INT_MAX, gr = 0;
+    for (int r = 0; r < CS; ++r)
+    {
+      const double v = sh.cand[par][r].val;
+      const int i = sh.cand[par][r].idx;
+      if (better(v, i, gv, gi))
+      {
+        gv = v;
+        gi = i;
+        gr = r;
+      }
+    }
+    const bool knan = sh.rowk[par].nan != 0;
+    const int p = knan ? k : gi;
+    const T *U = knan ? sh.rowk[par].row : sh.cand[par][gr].row;
+    const T piv = U[j];
+    if (rank == 0 && t == 0)
+    {
+      ipiv[k] = p;
+      if (!knan && gv == 0.0)
+        atomicMin(&info->singular_col, k);
+    }
+    if (p != k)
+    {
+      if (p >= row0 && p < row0 + mloc)
+      {
+        const int pl = p - row0;
+        if (pl % PANEL_THREADS == t)
+        {
+          for (int c = 0; c < jb; ++c)
+            P[c * R + pl] = sh.rowk[par].row[c];
+          rowid[pl] = sh.rowk[par].rowid;
+        }
+      }
+      if (own_k)
+      {
+        const int kl = k - row0;
+        if (kl % PANEL_THREADS == t)
+        {
+          for (int c = 0; c < jb; ++c)
+            P[c * R + kl] = U[c];
+          rowid[kl] = sh.cand[par][gr].rowid;
+        }
+      }
+    }
+
+    // Scale (true division, dense_lu.hpp:87-89), rank-1 update of the rest of
+    // the panel (dense_lu.hpp:91-107), and the candidate for column j+1.
+    bv = -1.0;
+    bi = INT_MAX;
+    for (int i = t; i < mloc; i += PANEL_THREADS)
+    {
+      const int g = row0 + i;
+      if (g <= k)
+        continue;
+      const T l = divide(P[j * R + i], piv);
+      P[j * R + i] = l;
+      for (int c = j + 1; c < jb; ++c)
+        P[c * R + i] = upd(P[c * R + i], l, U[c]);
+      if (j + 1 < jb)
+      {
+        const double a = fabs(to_d(P[(j + 1) * R + i]));
+        if (!isnan(a) && better(a, g, bv, bi))
+        {
+          bv = a;
+          bi = g;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < jb; ++c)
+  {
+    T *col = A + (size_t)(k0 + c) * n + row0;
+    for (int i = t; i < mloc; i += PANEL_THREADS)
+      col[i] = P[c * R + i];
+  }
+  for (int i = t; i < mloc; i += PANEL_THREADS)
+    if (rowid[i] != row0 + i)
+    {
+      const int q = atomicAdd(nmoves, 1);
+      moves[q] = make_int2(row0 + i, rowid[i]);
+    }
+  // No CTA may exit while others can still touch its shared memory.
+  cluster.sync();
+}
+
+// Gather-apply the panel's row moves (new[dst] = old[src]) to columns
+// [0, k0) and [k0+jb, n) -- one warp per column -- and to perm (block 0).
+template <typename T, int NB>
+__global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, int n, int k0,
+                                                             int jb, const int2 *__restrict__ moves,
+                                                             const int *__restrict__ nmoves,
+                                                             int *__restrict__ perm)
+{
+  constexpr int PER = (2 * NB + 31) / 32;
+  const int nm = *nmoves;
+  if (nm == 0)
+    return;
+  const int lane = threadIdx.x & 31;
+  int2 mv[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q)
+  {
+    const int e = lane + 32 * q;
+    mv[q] = e < nm ? moves[e] : make_int2(-1, -1);
+  }
+  const int ncols = n - jb;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  if (blockIdx.x == 0 && threadIdx.x < 32 && perm)
+  {
+    int v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      if (mv[q].x >= 0)
+        v[q] = perm[mv[q].y];
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      if (mv[q].x >= 0)
+        perm[mv[q].x] = v[q];
+  }
+  constexpr int UNR = 4;
+  for (int c0 = gw * UNR; c0 < ncols; c0 += nw * UNR)
+  {
+    T v[UNR][PER];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+    {
+      const int cc = c0 + u;
+      if (cc < ncols)
+      {
+        const int col = cc < k0 ? cc : cc + jb;
+        const T *cp = A + (size_t)col * n;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            v[u][q] = cp[mv[q].y];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+    {
+      const int cc = c0 + u;
+      if (cc < ncols)
+      {
+        const int col = cc < k0 ? cc : cc + jb;
+        T *cp = A + (size_t)col * n;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            cp[mv[q].x] = v[u][q];
+      }
+    }
+  }
+}
+
+// U12 = L11^{-1} A12 (unit lower), one thread per trailing column, k order.
+template <typename T, int NB>
+__global__ void __launch_bounds__(128) lu_trsm_kernel(T *__restrict__ A, int n, int k0, int jb)
+{
+  __shared__ T L[NB][NB + 1];
+  for (int idx = threadIdx.x; idx < jb * jb; idx += blockDim.x)
+  {
+    const int kk = idx / jb, i = idx % jb;
+    L[i][kk] = A[(size_t)(k0 + kk) * n + k0 + i];
+  }
+  __syncthreads();
+  const int col = k0 + jb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n)
+    return;
+  T *cp = A + (size_t)col * n + k0;
+  T x[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+    if (i < jb)
+      x[i] = cp[i];
+#pragma unroll
+  for (int kk = 0; kk < NB; ++kk)
+  {
+    if (kk >= jb)
+      break;
+#pragma unroll
+    for (int i = kk + 1; i < NB; ++i)
+      if (i < jb)
+        x[i] = upd(x[i], L[i][kk], x[kk]);
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+    if (i < jb)
+      cp[i] = x[i];
+}
+
+// ---- trailing update A22 -= L21 * U12 ------------------------------------
+// Compute type: binary16 values are held exactly in fp32 registers.
+template <typename T> struct CType { using type = T; };
+template <> struct CType<h16> { using type = float; };
+
+__device__ __forceinline__ float to_c(h16 v) { return h2f(v); }
+__device__ __forceinline__ float to_c(float v) { return v; }
+__device__ __forceinline__ double to_c(double v) { return v; }
+__device__ __forceinline__ void from_c(h16 &dst, float v) { dst = f2h(v); }
+__device__ __forceinline__ void from_c(float &dst, float v) { dst = v; }
+__device__ __forceinline__ void from_c(double &dst, double v) { dst = v; }
+
+template <typename T>
+__device__ __forceinline__ typename CType<T>::type gemm_upd(typename CType<T>::type c,
+                                                            typename CType<T>::type l,
+                                                            typename CType<T>::type u)
+{
+  if constexpr (std::is_same<T, h16>::value)
+  {
+    const float p = __half2float(__float2half_rn(__fmul_rn(l, u)));
+    return __half2float(__float2half_rn(__fsub_rn(c, p)));
+  }
+  else
+    return upd(c, l, u);
+}
+
+constexpr int GB = 128;       // C tile edge
+constexpr int GPAD = 4;       // Bs row padding
+template <typename T, int NB>
+constexpr size_t gemm_smem_bytes()
+{
+  using C = typename CType<T>::type;
+  return sizeof(C) * (size_t)NB * GB + sizeof(C) * (size_t)NB * (GB + GPAD);
+}
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, int k0, int jb)
+{
+  using C = typename CType<T>::type;
+  extern __shared__ __align__(16) unsigned char gsm[];
+  C *As = reinterpret_cast<C *>(gsm);                  // [NB][GB]
+  C *Bs = As + (size_t)NB * GB;                        // [NB][GB+GPAD]
+  const int c0 = k0 + jb;
+  const int r0 = c0 + blockIdx.x * GB;
+  const int cc0 = c0 + blockIdx.y * GB;
+  const int t = threadIdx.x;
+  const int tx = t & 15, ty = t >> 4;
+
+  for (int idx = t; idx < jb * GB; idx += 256)
+  {
+    const int kk = idx / GB, m = idx % GB;
+    const int row = r0 + m;
+    As[kk * GB + m] = row < n ? to_c(A[(size_t)(k0 + kk) * n + row]) : C(0);
+  }
+  for (int idx = t; idx < jb * GB; idx += 256)
+  {
+    const int nn = idx / jb, kk = idx % jb;
+    const int col = cc0 + nn;
+    Bs[kk * (GB + GPAD) + nn] = col < n ? to_c(A[(size_t)col * n + k0 + kk]) : C(0);
+  }
+
+  C acc[8][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+  {
+    const int col = cc0 + (j < 4 ? ty * 4 + j : 64 + ty * 4 + (j - 4));
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+    {
+      const int row = r0 + (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
+      acc[i][j] = (row < n && col < n) ? to_c(A[(size_t)col * n + row]) : C(0);
+    }
+  }
+  __syncthreads();
+
+  for (int kk = 0; kk < jb; ++kk)
+  {
+    C a[8], b[8];
+    const C *ar = As + kk * GB;
+    const C *br = Bs + kk * (GB + GPAD);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+    {
+      a[i] = ar[tx * 4 + i];
+      a[4 + i] = ar[64 + tx * 4 + i];
+      b[i] = br[ty * 4 + i];
+      b[4 + i] = br[64 + ty * 4 + i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        acc[i][j] = gemm_upd<T>(acc[i][j], a[i], b[j]);
+  }
+
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+  {
+    const int col = cc0 + (j < 4 ? ty * 4 + j : 64 + ty * 4 + (j - 4));
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+    {
+      const int row = r0 + (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
+      if (row < n && col < n)
+        from_c(A[(size_t)col * n + row], acc[i][j]);
+    }
+  }
+}
+
+__global__ void iota_kernel(int *p, int n)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = i;
+}
+
+__global__ void perm_from_ipiv_kernel(const int *__restrict__ ipiv, int n, int *__restrict__ perm)
+{
+  // Sequential by construction (apply_pivots order); n is small on this path.
+  if (threadIdx.x != 0)
+    return;
+  for (int i = 0; i < n; ++i)
+    perm[i] = i;
+  for (int k = 0; k < n; ++k)
+  {
+    const int p = ipiv[k];
+    if (p != k)
+    {
+      const int tmp = perm[k];
+      perm[k] = perm[p];
+      perm[p] = tmp;
+    }
+  }
+}
+
+// ---- host orchestration --------------------------------------------------
+template <typename T, int NB>
+struct PanelLaunch
+{
+  static bool configured;
+  static void configure()
+  {
+    if (configured)
+      return;
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_kernel<T, NB>,
+                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_kernel<T, NB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          220 * 1024));
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_kernel<T, NB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)gemm_smem_bytes<T, NB>()));
+    configured = true;
+  }
+};
+template <typename T, int NB>
+bool PanelLaunch<T, NB>::configured = false;
+
+template <typename T, int NB>
+void panel_geometry(int m, int &cs, int &R)
+{
+  cs = std::min(MAX_CLUSTER, std::max(1, (m + PANEL_THREADS - 1) / PANEL_THREADS));
+  R = (m + cs - 1) / cs;
+  while (panel_smem_bytes<T, NB>(R) > 220 * 1024)
+    throw std::runtime_error("LU panel does not fit in a 16-CTA cluster at this n; use a "
+                             "smaller nb");
+}
+
+template <typename T, int NB>
+void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, cudaStream_t s)
+{
+  PanelLaunch<T, NB>::configure();
+  if (perm)
+  {
+    iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(perm, n);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  }
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(ws.nmoves, 0, sizeof(int) * ws.npanels, s));
+  int sms = 148;
+  for (int p = 0, k0 = 0; k0 < n; ++p, k0 += NB)
+  {
+    const int jb = std::min(NB, n - k0);
+    const int m = n - k0;
+    int cs, R;
+    panel_geometry<T, NB>(m, cs, R);
+    int2 *mv = ws.moves + (size_t)p * 2 * NB;
+    int *nm = ws.nmoves + p;
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(PANEL_THREADS);
+    cfg.dynamicSmemBytes = panel_smem_bytes<T, NB>(R);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MPIRG_CUDA_CHECK(
+        cudaLaunchKernelEx(&cfg, lu_panel_kernel<T, NB>, a, n, k0, jb, R, ipiv, mv, nm, info));
+
+    const int ncols = n - jb;
+    if (ncols > 0)
+    {
+      const int warps_needed = (ncols + 3) / 4;
+      const int grid = std::max(1, std::min((warps_needed + 7) / 8, sms * 8));
+      lu_apply_moves_kernel<T, NB><<<grid, 256, 0, s>>>(a, n, k0, jb, mv, nm, perm);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+    }
+    else if (perm)
+    {
+      lu_apply_moves_kernel<T, NB><<<1, 32, 0, s>>>(a, n, k0, jb, mv, nm, perm);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+    }
+    const int nt = n - k0 - jb;
+    if (nt > 0)
+    {
+      lu_trsm_kernel<T, NB><<<(nt + 127) / 128, 128, 0, s>>>(a, n, k0, jb);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+      const int tiles = (nt + GB - 1) / GB;
+      lu_gemm_kernel<T, NB><<<dim3(tiles, tiles), 256, gemm_smem_bytes<T, NB>(), s>>>(a, n, k0,
+                                                                                     jb);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+    }
+  }
+}
+
+}  // namespace
+
+int lu_choose_nb(int prec, int n, int requested)
+{
+  if (requested == 32 || requested == 64)
+    return requested;
+  if (prec == B64)
+    return 32;
+  if (prec == B32)
+    return n <= 8192 ? 64 : 32;
+  return 64;
+}
+
+void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
+{
+  lu_workspace_free(ws);
+  ws.n = n;
+  ws.nb = lu_choose_nb(prec, n, nb);
+  ws.npanels = (n + ws.nb - 1) / ws.nb;
+  MPIRG_CUDA_CHECK(cudaMalloc(&ws.moves, sizeof(int2) * (size_t)ws.npanels * 2 * ws.nb));
+  MPIRG_CUDA_CHECK(cudaMalloc(&ws.nmoves, sizeof(int) * (size_t)ws.npanels));
+}
+
+void lu_workspace_free(LuWorkspace &ws)
+{
+  if (ws.moves)
+    cudaFree(ws.moves);
+  if (ws.nmoves)
+    cudaFree(ws.nmoves);
+  ws = LuWorkspace{};
+}
+
+void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWorkspace &ws,
+               DevInfo *info, cudaStream_t s)
+{
+  if (n <= 0)
+    return;
+  (void)lu_mode;
+  if (prec == B64)
+  {
+    if (ws.nb == 64)
+      lu_run<double, 64>(static_cast<double *>(a), n, ipiv, perm, ws, info, s);
+    else
+      lu_run<double, 32>(static_cast<double *>(a), n, ipiv, perm, ws, info, s);
+  }
+  else if (prec == B32)
+  {
+    if (ws.nb == 64)
+      lu_run<float, 64>(static_cast<float *>(a), n, ipiv, perm, ws, info, s);
+    else
+      lu_run<float, 32>(static_cast<float *>(a), n, ipiv, perm, ws, info, s);
+  }
+  else
+  {
+    if (ws.nb == 64)
+      lu_run<h16, 64>(static_cast<h16 *>(a), n, ipiv, perm, ws, info, s);
+    else
+      lu_run<h16, 32>(static_cast<h16 *>(a), n, ipiv, perm, ws, info, s);
+  }
+}
+
+void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s)
+{
+  perm_from_ipiv_kernel<<<1, 32, 0, s>>>(ipiv, n, perm);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace mpirg

@@ -1,0 +1,978 @@
+// Host side of the B200 IR hot path: the MPFactorization handle, the
+// refinement loop, and the C-ABI declared in include/mpir_gpu.h.
+//
+// Mirrors, line for line where it matters:
+//   resolve_config / PrecisionConfig::validate  mp_structures.hpp:44-59, precision.hpp:222-230
+//   MPFactorization ctor + refactor             mp_structures.hpp:108-169
+//   TermParams / update_parms                   ir_engine.hpp:29-64
+//   detail::plain_correction                    ir_engine.hpp:144-181
+//   detail::refine_loop (termination ledger)    ir_engine.hpp:186-271
+//   residual_tr                                 ir_engine.hpp:277-287
+// The loop runs on the host exactly as in the reference; each pass launches
+// the fused substitution pair and the residual kernel and reads back three
+// doubles (||d||, ||x||, ||r||) plus the non-finite flag.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mpir_gpu.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace mpirg;
+
+namespace
+{
+
+struct ApiError
+{
+  int status;
+  std::string msg;
+  int column = -1;
+  double value = 0.0;
+};
+
+const char *prec_name(int p) { return p == B64 ? "b64" : (p == B32 ? "b32" : "b16"); }
+bool at_least_as_wide(int p, int q) { return p <= q; }  // codes: 0 widest
+double machine_eps_of(int p) { return p == B64 ? 0x1p-52 : (p == B32 ? 0x1p-23 : 0x1p-10); }
+double max_finite_of(int p) { return p == B64 ? DBL_MAX : (p == B32 ? (double)FLT_MAX : 65504.0); }
+
+void validate_config(const mpirg_config &c)
+{
+  if (c.tw < 0 || c.tw > 2 || c.tf < 0 || c.tf > 2 || c.tr < 0 || c.tr > 2)
+    throw ApiError{MPIRG_ERR_INVALID_CONFIG, "unknown precision"};
+  if (c.tw == B16)
+    throw ApiError{MPIRG_ERR_INVALID_CONFIG, "working precision must be b64 or b32"};
+  if (!at_least_as_wide(c.tw, c.tf))
+    throw ApiError{MPIRG_ERR_INVALID_CONFIG,
+                   "factorization precision must not exceed the working precision"};
+  if (!at_least_as_wide(c.tr, c.tw))
+    throw ApiError{MPIRG_ERR_INVALID_CONFIG,
+                   "residual precision must be at least the working precision"};
+  if (c.tr == B16)
+    throw ApiError{MPIRG_ERR_INVALID_CONFIG, "residual precision must be b64 or b32"};
+  if (c.tf == c.tw && !c.on_the_fly)
+    throw ApiError{MPIRG_ERR_INVALID_CONFIG, "equal-precision factors require on-the-fly solves"};
+  if (c.lu_mode == MPIRG_LU_TC && c.tf != B16)
+    throw ApiError{MPIRG_ERR_INVALID_CONFIG, "tensor-core LU needs binary16 factors"};
+}
+
+void validate_term(const mpirg_term_params &t)
+{
+  if (!(t.cr > 0.0) || !std::isfinite(t.cr))
+    throw ApiError{MPIRG_ERR_INVALID_PARAM, "cr must be positive and finite"};
+  if (!(t.ce > 0.0) || !std::isfinite(t.ce))
+    throw ApiError{MPIRG_ERR_INVALID_PARAM, "ce must be positive and finite"};
+  if (!(t.rmax > 0.0) || !(t.rmax <= 1.0))
+    throw ApiError{MPIRG_ERR_INVALID_PARAM, "rmax must lie in (0, 1]"};
+  if (t.litmax < 1)
+    throw ApiError{MPIRG_ERR_INVALID_PARAM, "litmax must be at least 1"};
+}
+
+double bits_to_d(unsigned long long b)
+{
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+void fill_err(mpirg_error *err, int status, const std::string &msg, int column = -1,
+              double value = 0.0)
+{
+  if (!err)
+    return;
+  err->status = status;
+  err->column = column;
+  err->value = value;
+  std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+}
+
+template <typename F>
+int guarded(mpirg_error *err, F &&fn)
+{
+  try
+  {
+    fn();
+    fill_err(err, MPIRG_OK, "");
+    return MPIRG_OK;
+  }
+  catch (const ApiError &e)
+  {
+    fill_err(err, e.status, e.msg, e.column, e.value);
+    return e.status;
+  }
+  catch (const CudaError &e)
+  {
+    fill_err(err, MPIRG_ERR_CUDA, e.what());
+    return MPIRG_ERR_CUDA;
+  }
+  catch (const std::invalid_argument &e)
+  {
+    fill_err(err, MPIRG_ERR_INVALID_CONFIG, e.what());
+    return MPIRG_ERR_INVALID_CONFIG;
+  }
+  catch (const std::exception &e)
+  {
+    fill_err(err, MPIRG_ERR_CUDA, e.what());
+    return MPIRG_ERR_CUDA;
+  }
+}
+
+void require_gpu()
+{
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw ApiError{MPIRG_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)"};
+}
+
+template <typename T>
+T *dalloc(size_t count)
+{
+  void *p = nullptr;
+  MPIRG_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  return static_cast<T *>(p);
+}
+void *dalloc_bytes(size_t bytes)
+{
+  void *p = nullptr;
+  MPIRG_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  return p;
+}
+
+void reset_info(DevInfo *info, cudaStream_t s)
+{
+  DevInfo h;
+  h.overflow_index = ~0ull;
+  h.underflow = 0;
+  h.singular_col = INT_MAX;
+  h.nonfinite = 0;
+  h.pad = 0;
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(info, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// The handle
+// ---------------------------------------------------------------------------
+struct mpirg_factorization
+{
+  int n = 0;
+  mpirg_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void *a_high = nullptr;  // TW
+  void *a_low = nullptr;   // TF: packed LU
+  int *ipiv = nullptr;
+  int *perm = nullptr;
+  void *b = nullptr;       // TW
+  void *r = nullptr;       // TR
+  void *x = nullptr;       // TR
+  void *y = nullptr;       // substitution scratch (max(TW, TF) bytes)
+  void *sol = nullptr;     // TW
+  unsigned long long *scal = nullptr;  // [0] ||A||_1, [1] ||b||, [2+3i..] per pass
+  int scal_cap = 0;
+  DevInfo *info = nullptr;
+  DevInfo *h_info = nullptr;               // pinned
+  unsigned long long *h_scal = nullptr;    // pinned
+  LuWorkspace luws;
+  TrsvWorkspace tws;
+  ResidualPlan rplan;
+  double anorm1 = 0.0;
+  int underflow = 0;
+  float factor_ms = 0.0f;
+  cudaEvent_t ev[4] = {};
+
+  size_t tw_bytes() const { return elem_size(cfg.tw); }
+  size_t tf_bytes() const { return elem_size(cfg.tf); }
+  size_t tr_bytes() const { return elem_size(cfg.tr); }
+  bool ext() const { return cfg.tr != cfg.tw; }
+
+  void ensure_scal(int litmax)
+  {
+    const int need = 2 + 3 * (litmax + 1);
+    if (need <= scal_cap)
+      return;
+    if (scal)
+      cudaFree(scal);
+    if (h_scal)
+      cudaFreeHost(h_scal);
+    scal = dalloc<unsigned long long>(need);
+    MPIRG_CUDA_CHECK(cudaMallocHost(&h_scal, sizeof(unsigned long long) * need));
+    scal_cap = need;
+  }
+
+  void alloc()
+  {
+    const size_t nn = (size_t)n * n;
+    MPIRG_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    a_high = dalloc_bytes(nn * tw_bytes());
+    a_low = dalloc_bytes(nn * tf_bytes());
+    ipiv = dalloc<int>(n);
+    perm = dalloc<int>(n);
+    b = dalloc_bytes(n * tw_bytes());
+    r = dalloc_bytes(n * tr_bytes());
+    x = dalloc_bytes(n * tr_bytes());
+    y = dalloc_bytes(n * 8);
+    sol = dalloc_bytes(n * tw_bytes());
+    info = dalloc<DevInfo>(1);
+    MPIRG_CUDA_CHECK(cudaMallocHost(&h_info, sizeof(DevInfo)));
+    ensure_scal(16);
+    lu_workspace_alloc(luws, cfg.tf, n, cfg.nb);
+    trsv_workspace_alloc(tws, n);
+    residual_plan_make(rplan, cfg.tw, n, a_high);
+    for (auto &e : ev)
+      MPIRG_CUDA_CHECK(cudaEventCreate(&e));
+  }
+
+  void release()
+  {
+    cudaSetDevice(device);
+    for (void *p : {a_high, a_low, (void *)ipiv, (void *)perm, b, r, x, y, sol, (void *)scal,
+                    (void *)info})
+      if (p)
+        cudaFree(p);
+    if (h_info)
+      cudaFreeHost(h_info);
+    if (h_scal)
+      cudaFreeHost(h_scal);
+    lu_workspace_free(luws);
+    trsv_workspace_free(tws);
+    residual_plan_free(rplan);
+    for (auto &e : ev)
+      if (e)
+        cudaEventDestroy(e);
+    if (stream)
+      cudaStreamDestroy(stream);
+  }
+
+  // MPFactorization::refactor (mp_structures.hpp:155-169).
+  void refactor()
+  {
+    cudaStream_t s = stream;
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    reset_info(info, s);
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(scal, 0, sizeof(unsigned long long), s));
+    launch_cast_norm(cfg.tw, cfg.tf, n, n, a_high, a_low, scal, info, s);
+    launch_lu(cfg.tf, cfg.lu_mode, a_low, n, ipiv, perm, luws, info, s);
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[1], s));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(h_info, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
+    MPIRG_CUDA_CHECK(
+        cudaMemcpyAsync(h_scal, scal, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+    MPIRG_CUDA_CHECK(cudaEventElapsedTime(&factor_ms, ev[0], ev[1]));
+    anorm1 = bits_to_d(h_scal[0]);
+    underflow = h_info->underflow;
+    if (h_info->overflow_index != ~0ull)
+    {
+      double v = 0.0;
+      const size_t idx = (size_t)h_info->overflow_index;
+      if (cfg.tw == B64)
+        MPIRG_CUDA_CHECK(cudaMemcpy(&v, (char *)a_high + idx * 8, 8, cudaMemcpyDeviceToHost));
+      else
+      {
+        float f;
+        MPIRG_CUDA_CHECK(cudaMemcpy(&f, (char *)a_high + idx * 4, 4, cudaMemcpyDeviceToHost));
+        v = f;
+      }
+      throw ApiError{MPIRG_ERR_OVERFLOW,
+                     "value " + std::to_string(v) + " exceeds the largest finite " +
+                         prec_name(cfg.tf) + " value",
+                     -1, v};
+    }
+    if (h_info->singular_col != INT_MAX)
+      throw ApiError{MPIRG_ERR_SINGULAR, "pivot column is exactly zero", h_info->singular_col};
+  }
+
+  // detail::refine_loop + plain_correction (ir_engine.hpp:144-271).
+  void solve(const mpirg_term_params &tp, mpirg_report *rep)
+  {
+    validate_term(tp);
+    ensure_scal(tp.litmax);
+    cudaStream_t s = stream;
+    const int ns = 2 + 3 * (tp.litmax + 1);
+    std::vector<double> rhist, dhist;
+    rhist.reserve(tp.litmax + 1);
+    dhist.reserve(tp.litmax + 1);
+    auto emit = [&](int reason) {
+      rep->rhist_len = (int)rhist.size();
+      rep->dhist_len = (int)dhist.size();
+      const int cap = rep->hist_capacity;
+      for (int i = 0; i < (int)rhist.size() && i < cap; ++i)
+        rep->rhist[i] = rhist[i];
+      for (int i = 0; i < (int)dhist.size() && i < cap; ++i)
+        rep->dhist[i] = dhist[i];
+      rep->reason = reason;
+    };
+
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[2], s));
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(scal + 1, 0, sizeof(unsigned long long) * (ns - 1), s));
+    reset_info(info, s);
+    launch_ir_init(cfg.tw, cfg.tr, n, b, r, x, scal + 1, s);
+
+    const bool extended = ext();
+    const double eps_w = machine_eps_of(cfg.tw);
+    double bnorm = 0.0, rnorm = 0.0;
+    int reason = MPIRG_ITERATION_LIMIT;
+    for (int it = 0;; ++it)
+    {
+      unsigned long long *slot = scal + 2 + 3 * it;
+      TrsvArgs a{};
+      a.n = n;
+      a.lu = a_low;
+      a.perm = perm;
+      a.rin = r;
+      a.y = y;
+      a.out = x;
+      a.ir = 1;
+      a.tin = cfg.tr;
+      a.tf = cfg.tf;
+      a.dnorm_bits = slot + 0;
+      a.xnorm_bits = slot + 1;
+      a.info = info;
+      if (cfg.on_the_fly)
+      {
+        a.ts = cfg.tw;  // solve_mps_into<TW,TF> (on TW(r) when TR > TW)
+        a.lps = 0;
+      }
+      else
+      {
+        a.ts = cfg.tf;  // solve_lps_into<TR,TF>
+        a.lps = 1;
+        a.rho_bits = it == 0 ? scal + 1 : scal + 2 + 3 * (it - 1) + 2;
+      }
+      launch_trsv(a, tws, s);
+      launch_residual(rplan, cfg.tr, x, b, r, slot + 2, s);
+      const int nread = 2 + 3 * (it + 1);
+      MPIRG_CUDA_CHECK(cudaMemcpyAsync(h_scal + 1, scal + 1,
+                                       sizeof(unsigned long long) * (nread - 1),
+                                       cudaMemcpyDeviceToHost, s));
+      MPIRG_CUDA_CHECK(
+          cudaMemcpyAsync(h_info, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
+      MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+
+      if (it == 0)
+      {
+        bnorm = bits_to_d(h_scal[1]);
+        rhist.push_back(bnorm);
+        if (!std::isfinite(bnorm))
+        {
+          emit(MPIRG_ITERATION_LIMIT);
+          throw ApiError{MPIRG_ERR_NONFINITE, "right-hand side is not finite"};
+        }
+        rnorm = bnorm;
+      }
+      if (h_info->nonfinite)
+      {
+        emit(MPIRG_ITERATION_LIMIT);
+        throw ApiError{MPIRG_ERR_NONFINITE,
+                       cfg.on_the_fly ? "promoting substitution produced a non-finite entry"
+                                      : "scaled substitution produced a non-finite entry"};
+      }
+      const unsigned long long *hs = h_scal + 2 + 3 * it;
+      const double dnorm = bits_to_d(hs[0]);
+      const double xnorm = bits_to_d(hs[1]);
+      const double rnew = bits_to_d(hs[2]);
+      dhist.push_back(dnorm);
+      rhist.push_back(rnew);
+      if (!std::isfinite(rnew) || !std::isfinite(dnorm))
+      {
+        emit(MPIRG_ITERATION_LIMIT);
+        throw ApiError{MPIRG_ERR_NONFINITE, "refinement produced a non-finite iterate"};
+      }
+      if (!extended)
+      {
+        const bool small = cfg.resid_term ? rnew <= tp.cr * eps_w * bnorm
+                                          : rnew <= tp.ce * eps_w * (bnorm + anorm1 * xnorm);
+        if (small)
+        {
+          reason = cfg.resid_term ? MPIRG_SMALL_RESIDUAL : MPIRG_SMALL_BACKWARD_ERROR;
+          break;
+        }
+        if (rnew >= tp.rmax * rnorm)
+        {
+          reason = MPIRG_RESIDUAL_STAGNATION;
+          break;
+        }
+      }
+      else
+      {
+        const size_t k = dhist.size();
+        if (k >= 2 && dhist[k - 1] >= tp.rmax * dhist[k - 2])
+        {
+          reason = MPIRG_CORRECTION_STAGNATION;
+          break;
+        }
+      }
+      if ((int)rhist.size() >= tp.litmax)
+      {
+        reason = MPIRG_ITERATION_LIMIT;
+        break;
+      }
+      rnorm = rnew;
+    }
+    launch_ir_finish(cfg.tw, cfg.tr, n, x, sol, s);
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[3], s));
+    if (rep->sol)
+      MPIRG_CUDA_CHECK(cudaMemcpyAsync(rep->sol, sol, n * tw_bytes(),
+                                       rep->sol_on_device ? cudaMemcpyDeviceToDevice
+                                                          : cudaMemcpyDeviceToHost,
+                                       s));
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0.0f;
+    MPIRG_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+    rep->solve_ms = ms;
+    emit(reason);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Shared context for the kernel-level entry points (one per device).
+// ---------------------------------------------------------------------------
+namespace
+{
+
+struct KernelCtx
+{
+  DevInfo *info = nullptr;
+  DevInfo *h_info = nullptr;
+  unsigned long long *bits = nullptr;
+  LuWorkspace luws;
+  int lu_prec = -1, lu_nb = -1;
+  TrsvWorkspace tws;
+  int *perm = nullptr;
+  int perm_n = 0;
+};
+
+std::mutex g_mu;
+KernelCtx g_ctx[64];
+
+KernelCtx &ctx_for_current()
+{
+  int dev = 0;
+  MPIRG_CUDA_CHECK(cudaGetDevice(&dev));
+  KernelCtx &c = g_ctx[dev & 63];
+  if (!c.info)
+  {
+    c.info = dalloc<DevInfo>(1);
+    c.bits = dalloc<unsigned long long>(4);
+    MPIRG_CUDA_CHECK(cudaMallocHost(&c.h_info, sizeof(DevInfo)));
+  }
+  return c;
+}
+
+int *ctx_perm(KernelCtx &c, int n)
+{
+  if (c.perm_n < n)
+  {
+    if (c.perm)
+      cudaFree(c.perm);
+    c.perm = dalloc<int>(n);
+    c.perm_n = n;
+  }
+  return c.perm;
+}
+
+DevInfo read_info(KernelCtx &c, cudaStream_t s)
+{
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(c.h_info, c.info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
+  MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+  return *c.h_info;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int mpirg_abi_version(void) { return MPIRG_ABI_VERSION; }
+
+int mpirg_device_count(void)
+{
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess)
+  {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+double mpirg_machine_eps(int p) { return machine_eps_of(p); }
+double mpirg_unit_roundoff(int p) { return p == B64 ? 0x1p-53 : (p == B32 ? 0x1p-24 : 0x1p-11); }
+
+int mpirg_resolve_config(int tw, int tf, int tr, int on_the_fly, mpirg_config *out,
+                         mpirg_error *err)
+{
+  return guarded(err, [&] {
+    if (tw == B16)
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG, "working precision must be b64 or b32"};
+    if (tw < 0 || tw > 2)
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG, "unknown precision"};
+    mpirg_config c{};
+    c.tw = tw;
+    c.tr = tr >= 0 ? tr : tw;
+    c.tf = tf >= 0 ? tf : (tw == B32 ? B16 : B32);
+    c.on_the_fly = on_the_fly >= 0 ? on_the_fly : (c.tf == B16);
+    if (c.tf == c.tw)
+      c.on_the_fly = 1;
+    c.resid_term = 1;
+    c.lu_mode = MPIRG_LU_EXACT;
+    c.nb = 0;
+    c.device = -1;
+    validate_config(c);
+    *out = c;
+  });
+}
+
+int mpirg_update_parms(double cr, double ce, double rmax, int litmax, mpirg_term_params *out,
+                       mpirg_error *err)
+{
+  return guarded(err, [&] {
+    mpirg_term_params t{1.0, 1.0, 0.5, 10};
+    if (!std::isnan(cr))
+      t.cr = cr;
+    if (!std::isnan(ce))
+      t.ce = ce;
+    if (!std::isnan(rmax))
+      t.rmax = rmax;
+    if (litmax > 0)
+      t.litmax = litmax;
+    validate_term(t);
+    *out = t;
+  });
+}
+
+int mpirg_factorization_create(mpirg_factorization **out, int n, const mpirg_config *cfg_in,
+                               const void *a, int a_on_device, mpirg_error *err)
+{
+  *out = nullptr;
+  return guarded(err, [&] {
+    if (n < 0)
+      throw ApiError{MPIRG_ERR_INVALID_SIZE, "matrix dimensions must be nonnegative"};
+    mpirg_config c = *cfg_in;
+    // mp_structures.hpp:118-122
+    if (c.on_the_fly < 0)
+      c.on_the_fly = (c.tf == B16 || c.tf == c.tw);
+    if (c.tf == c.tw)
+      c.on_the_fly = 1;
+    validate_config(c);
+    require_gpu();
+    auto *f = new mpirg_factorization;
+    f->n = n;
+    f->cfg = c;
+    if (c.device >= 0)
+      MPIRG_CUDA_CHECK(cudaSetDevice(c.device));
+    MPIRG_CUDA_CHECK(cudaGetDevice(&f->device));
+    f->cfg.device = f->device;
+    try
+    {
+      f->alloc();
+      if (n > 0)
+      {
+        MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->a_high, a, (size_t)n * n * f->tw_bytes(),
+                                         a_on_device ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyHostToDevice,
+                                         f->stream));
+        f->refactor();
+      }
+    }
+    catch (...)
+    {
+      f->release();
+      delete f;
+      throw;
+    }
+    *out = f;
+  });
+}
+
+int mpirg_factorization_refactor(mpirg_factorization *f, const void *a, int a_on_device,
+                                 mpirg_error *err)
+{
+  return guarded(err, [&] {
+    MPIRG_CUDA_CHECK(cudaSetDevice(f->device));
+    if (a)
+      MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->a_high, a, (size_t)f->n * f->n * f->tw_bytes(),
+                                       a_on_device ? cudaMemcpyDeviceToDevice
+                                                   : cudaMemcpyHostToDevice,
+                                       f->stream));
+    if (f->n > 0)
+      f->refactor();
+  });
+}
+
+void mpirg_factorization_destroy(mpirg_factorization *f)
+{
+  if (!f)
+    return;
+  f->release();
+  delete f;
+}
+
+int mpirg_factorization_n(const mpirg_factorization *f) { return f->n; }
+int mpirg_factorization_config(const mpirg_factorization *f, mpirg_config *out)
+{
+  *out = f->cfg;
+  return MPIRG_OK;
+}
+double mpirg_factorization_a_norm1(const mpirg_factorization *f) { return f->anorm1; }
+int mpirg_factorization_demotion_underflowed(const mpirg_factorization *f) { return f->underflow; }
+size_t mpirg_factorization_matrix_bytes(const mpirg_factorization *f)
+{
+  return (size_t)f->n * f->n * (f->tw_bytes() + f->tf_bytes());
+}
+double mpirg_factorization_last_factor_ms(const mpirg_factorization *f) { return f->factor_ms; }
+
+int mpirg_factorization_get_ipiv(const mpirg_factorization *f, int *ipiv)
+{
+  cudaSetDevice(f->device);
+  return cudaMemcpy(ipiv, f->ipiv, sizeof(int) * f->n, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? MPIRG_OK
+             : MPIRG_ERR_CUDA;
+}
+int mpirg_factorization_get_pivots(const mpirg_factorization *f, int *perm)
+{
+  cudaSetDevice(f->device);
+  return cudaMemcpy(perm, f->perm, sizeof(int) * f->n, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? MPIRG_OK
+             : MPIRG_ERR_CUDA;
+}
+int mpirg_factorization_get_packed_lu(const mpirg_factorization *f, void *out)
+{
+  cudaSetDevice(f->device);
+  return cudaMemcpy(out, f->a_low, (size_t)f->n * f->n * f->tf_bytes(),
+                    cudaMemcpyDeviceToHost) == cudaSuccess
+             ? MPIRG_OK
+             : MPIRG_ERR_CUDA;
+}
+int mpirg_factorization_get_a_high(const mpirg_factorization *f, void *out)
+{
+  cudaSetDevice(f->device);
+  return cudaMemcpy(out, f->a_high, (size_t)f->n * f->n * f->tw_bytes(),
+                    cudaMemcpyDeviceToHost) == cudaSuccess
+             ? MPIRG_OK
+             : MPIRG_ERR_CUDA;
+}
+const void *mpirg_factorization_a_high_device(const mpirg_factorization *f) { return f->a_high; }
+const void *mpirg_factorization_packed_lu_device(const mpirg_factorization *f) { return f->a_low; }
+const int *mpirg_factorization_ipiv_device(const mpirg_factorization *f) { return f->ipiv; }
+void *mpirg_factorization_stream(const mpirg_factorization *f) { return f->stream; }
+
+int mpirg_ir_solve(mpirg_factorization *f, const void *b, int b_on_device,
+                   const mpirg_term_params *tp, mpirg_report *rep, mpirg_error *err)
+{
+  rep->rhist_len = 0;
+  rep->dhist_len = 0;
+  return guarded(err, [&] {
+    mpirg_term_params t = tp ? *tp : mpirg_term_params{1.0, 1.0, 0.5, 10};
+    MPIRG_CUDA_CHECK(cudaSetDevice(f->device));
+    if (f->n == 0)
+    {
+      validate_term(t);
+      rep->rhist_len = 0;
+      rep->reason = MPIRG_ITERATION_LIMIT;
+      return;
+    }
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->b, b, f->n * f->tw_bytes(),
+                                     b_on_device ? cudaMemcpyDeviceToDevice
+                                                 : cudaMemcpyHostToDevice,
+                                     f->stream));
+    f->solve(t, rep);
+  });
+}
+
+int mpirg_residual_tr(mpirg_factorization *f, const void *x, const void *b, void *r,
+                      int on_device, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    MPIRG_CUDA_CHECK(cudaSetDevice(f->device));
+    const int n = f->n;
+    cudaStream_t s = f->stream;
+    const cudaMemcpyKind in = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    // x (TW) -> sol scratch, widen into f->x (TR); b -> f->b.
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->sol, x, n * f->tw_bytes(), in, s));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->b, b, n * f->tw_bytes(), in, s));
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(f->scal + 1, 0, 2 * sizeof(unsigned long long), s));
+    launch_ir_init(f->cfg.tw, f->cfg.tr, n, f->sol, f->x, f->r, f->scal + 1, s);
+    launch_residual(f->rplan, f->cfg.tr, f->x, f->b, f->r, f->scal + 2, s);
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(r, f->r, n * f->tr_bytes(),
+                                     on_device ? cudaMemcpyDeviceToDevice
+                                               : cudaMemcpyDeviceToHost,
+                                     s));
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+// ---- kernel-level entry points ----------------------------------------------
+int mpirg_demote(int from, int to, size_t count, const void *src, void *dst, int *underflow,
+                 void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    require_gpu();
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto s = static_cast<cudaStream_t>(stream);
+    KernelCtx &c = ctx_for_current();
+    reset_info(c.info, s);
+    launch_demote(from, to, src, dst, count, c.info, s);
+    const DevInfo h = read_info(c, s);
+    if (underflow)
+      *underflow = h.underflow;
+    if (h.overflow_index != ~0ull)
+    {
+      double v = 0.0;
+      const size_t idx = (size_t)h.overflow_index;
+      if (from == B64)
+        MPIRG_CUDA_CHECK(cudaMemcpy(&v, (const char *)src + idx * 8, 8, cudaMemcpyDeviceToHost));
+      else
+      {
+        float fv;
+        MPIRG_CUDA_CHECK(cudaMemcpy(&fv, (const char *)src + idx * 4, 4, cudaMemcpyDeviceToHost));
+        v = fv;
+      }
+      throw ApiError{MPIRG_ERR_OVERFLOW,
+                     "value " + std::to_string(v) + " exceeds the largest finite " +
+                         prec_name(to) + " value",
+                     -1, v};
+    }
+  });
+}
+
+int mpirg_one_norm(int prec, int rows, int cols, const void *a, double *out, void *stream,
+                   mpirg_error *err)
+{
+  return guarded(err, [&] {
+    require_gpu();
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto s = static_cast<cudaStream_t>(stream);
+    KernelCtx &c = ctx_for_current();
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(c.bits, 0, sizeof(unsigned long long), s));
+    launch_one_norm(prec, rows, cols, a, c.bits, s);
+    unsigned long long hb = 0;
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(&hb, c.bits, 8, cudaMemcpyDeviceToHost, s));
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+    *out = bits_to_d(hb);
+  });
+}
+
+int mpirg_lu_factor(int prec, int n, void *a, int *ipiv, int lu_mode, int nb, void *stream,
+                    mpirg_error *err)
+{
+  return guarded(err, [&] {
+    require_gpu();
+    if (lu_mode == MPIRG_LU_TC && prec != B16)
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG, "tensor-core LU needs binary16 factors"};
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto s = static_cast<cudaStream_t>(stream);
+    KernelCtx &c = ctx_for_current();
+    const int want_nb = lu_choose_nb(prec, n, nb);
+    if (c.luws.n < n || c.lu_nb != want_nb || c.lu_prec != prec)
+    {
+      lu_workspace_alloc(c.luws, prec, n, nb);
+      c.lu_prec = prec;
+      c.lu_nb = c.luws.nb;
+    }
+    LuWorkspace ws = c.luws;  // sized for >= n panels
+    ws.n = n;
+    ws.npanels = (n + ws.nb - 1) / ws.nb;
+    reset_info(c.info, s);
+    launch_lu(prec, lu_mode, a, n, ipiv, nullptr, ws, c.info, s);
+    const DevInfo h = read_info(c, s);
+    if (h.singular_col != INT_MAX)
+      throw ApiError{MPIRG_ERR_SINGULAR, "pivot column is exactly zero", h.singular_col};
+  });
+}
+
+static void standalone_trsv(TrsvArgs &a, KernelCtx &c, cudaStream_t s)
+{
+  if (c.tws.n < a.n)
+    trsv_workspace_alloc(c.tws, a.n);
+  TrsvWorkspace ws = c.tws;
+  ws.n = a.n;
+  ws.nblk = (a.n + 31) / 32;
+  launch_trsv(a, ws, s);
+  c.tws.epoch = ws.epoch;
+}
+
+int mpirg_solve_mps(int ts, int tf, int n, const void *packed, const int *ipiv, void *x,
+                    void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    require_gpu();
+    if (!at_least_as_wide(ts, tf))
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG, "promotion must not lose precision"};
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto s = static_cast<cudaStream_t>(stream);
+    KernelCtx &c = ctx_for_current();
+    if (n == 0)
+      return;
+    int *perm = ctx_perm(c, n);
+    launch_perm_from_ipiv(ipiv, n, perm, s);
+    reset_info(c.info, s);
+    // Gather into scratch y first (the epilogue writes x in place).
+    void *xin = dalloc_bytes((size_t)n * elem_size(ts));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(xin, x, (size_t)n * elem_size(ts), cudaMemcpyDeviceToDevice, s));
+    void *y = dalloc_bytes((size_t)n * 8);
+    TrsvArgs a{};
+    a.ts = ts;
+    a.tf = tf;
+    a.tin = ts;
+    a.lps = 0;
+    a.ir = 0;
+    a.n = n;
+    a.lu = packed;
+    a.perm = perm;
+    a.rin = xin;
+    a.y = y;
+    a.out = x;
+    a.info = c.info;
+    standalone_trsv(a, c, s);
+    const DevInfo h = read_info(c, s);
+    cudaFree(xin);
+    cudaFree(y);
+    if (h.nonfinite)
+      throw ApiError{MPIRG_ERR_NONFINITE, "promoting substitution produced a non-finite entry"};
+  });
+}
+
+int mpirg_solve_lps(int tw, int tf, int n, const void *packed, const int *ipiv, void *r_to_d,
+                    void *scratch, int *underflow, void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    require_gpu();
+    if (!at_least_as_wide(tw, tf) || tw == B16)
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG, "demotion must not gain precision"};
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto s = static_cast<cudaStream_t>(stream);
+    KernelCtx &c = ctx_for_current();
+    if (n == 0)
+      return;
+    int *perm = ctx_perm(c, n);
+    launch_perm_from_ipiv(ipiv, n, perm, s);
+    reset_info(c.info, s);
+    // rho = max |r_i| with a > rho (NaN ignored): dense_lu.hpp:208-214.
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(c.bits, 0, sizeof(unsigned long long), s));
+    launch_one_norm(tw, 1, n, r_to_d, c.bits, s);  // max over "columns" of |r_i|, NaN ignored
+    void *rin = dalloc_bytes((size_t)n * elem_size(tw));
+    MPIRG_CUDA_CHECK(
+        cudaMemcpyAsync(rin, r_to_d, (size_t)n * elem_size(tw), cudaMemcpyDeviceToDevice, s));
+    TrsvArgs a{};
+    a.ts = tf;
+    a.tf = tf;
+    a.tin = tw;
+    a.lps = 1;
+    a.ir = 0;
+    a.n = n;
+    a.lu = packed;
+    a.perm = perm;
+    a.rin = rin;
+    a.rho_bits = c.bits;
+    a.y = scratch;
+    a.out = r_to_d;
+    a.info = c.info;
+    standalone_trsv(a, c, s);
+    const DevInfo h = read_info(c, s);
+    cudaFree(rin);
+    if (underflow)
+      *underflow = h.underflow;
+    if (h.nonfinite)
+      throw ApiError{MPIRG_ERR_NONFINITE, "scaled substitution produced a non-finite entry"};
+  });
+}
+
+int mpirg_residual(int tw, int tr, int n, const void *a, const void *x, const void *b, void *r,
+                   void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    require_gpu();
+    if (!at_least_as_wide(tr, tw) || tw == B16 || tr == B16)
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG,
+                     "residual precision must be at least the working precision"};
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto s = static_cast<cudaStream_t>(stream);
+    KernelCtx &c = ctx_for_current();
+    if (n == 0)
+      return;
+    ResidualPlan p;
+    residual_plan_make(p, tw, n, a);
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(c.bits, 0, sizeof(unsigned long long), s));
+    launch_residual(p, tr, x, b, r, c.bits, s);
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+    residual_plan_free(p);
+  });
+}
+
+int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *a, const void *b,
+                         int on_device, const mpirg_term_params *tp, void *sol, double *rhist,
+                         double *dhist, int hist_capacity, int *rhist_len, int *reason,
+                         int *status, double *device_ms, mpirg_error *err)
+{
+  int first = MPIRG_OK;
+  mpirg_error local{};
+  mpirg_factorization *f = nullptr;
+  mpirg_config c = *cfg;
+  const size_t tw = elem_size(c.tw);
+  double ms = 0.0;
+  for (int sidx = 0; sidx < count; ++sidx)
+  {
+    const char *as = static_cast<const char *>(a) + (size_t)sidx * n * n * tw;
+    const char *bs = static_cast<const char *>(b) + (size_t)sidx * n * tw;
+    int st;
+    if (!f)
+    {
+      st = mpirg_factorization_create(&f, n, &c, as, on_device, &local);
+      if (!f)
+      {
+        status[sidx] = st;
+        if (first == MPIRG_OK)
+        {
+          first = st;
+          if (err)
+            *err = local;
+        }
+        continue;
+      }
+    }
+    else
+      st = mpirg_factorization_refactor(f, as, on_device, &local);
+    if (st == MPIRG_OK)
+    {
+      ms += f->factor_ms;
+      mpirg_report rep{};
+      rep.sol = static_cast<char *>(sol) + (size_t)sidx * n * tw;
+      rep.sol_on_device = on_device;
+      rep.rhist = rhist + (size_t)sidx * hist_capacity;
+      rep.dhist = dhist + (size_t)sidx * hist_capacity;
+      rep.hist_capacity = hist_capacity;
+      st = mpirg_ir_solve(f, bs, on_device, tp, &rep, &local);
+      rhist_len[sidx] = rep.rhist_len;
+      reason[sidx] = rep.reason;
+      ms += rep.solve_ms;
+    }
+    status[sidx] = st;
+    if (st != MPIRG_OK && first == MPIRG_OK)
+    {
+      first = st;
+      if (err)
+        *err = local;
+    }
+  }
+  mpirg_factorization_destroy(f);
+  if (device_ms)
+    *device_ms = ms;
+  if (first == MPIRG_OK)
+    fill_err(err, MPIRG_OK, "");
+  return first;
+}
+
+}  // extern "C"
