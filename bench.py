@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""bench.py -- IR time-to-solution on B200 (BASELINE.json configs[1], config 2a).
+
+Workload (one "step"): the reference's factor-once + refine path on
+A = I - 800 G (N = 4096, trapezoid Green's operator, fp64), b ~ N(0,1) seed 0,
+<TW,TF,TR> = <fp64, fp32, fp64>, scaled (LPS) corrections, backward-error
+stopping rule with ce = 10, litmax = 20:
+    MPFactorization ctor work (||A||_1 + demotion + fp32 LU)  + ir_solve_report
+A is resident in HBM when the timed region starts (``value``); ``e2e`` goes
+through the public C-ABI with pinned HOST buffers, H2D of A and b and D2H of x
+inside the timed region.
+
+Metric (BASELINE.json): IR time-to-solution in seconds (lower is better);
+the LU GFLOP/s (2N^3/3 over the LU device time) rides along.
+
+--impl reference times the reference's own CPU code path (oracle/_ref: the
+unmodified reference headers compiled from /root/reference with its flags),
+single-threaded by construction for fp32 factors (mp_structures.hpp:166-167).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT = 4096
+ALPHA = 800.0
+CE, LITMAX = 10.0, 20
+METRIC = "IR time-to-solution & LU GFLOP/s (2N^3/3) vs fp16-TC/fp32 peak"
+HBM_FALLBACK = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def inputs(n):
+    """Seeded host inputs shared by every arm (cfg 2a)."""
+    import numpy as np
+    from paper_2311_14616_b200 import lib
+    L = lib()
+    a = np.empty(n * n, dtype=np.float64)  # column-major storage
+    L.mpirg_gen_greens_operator(n, ALPHA, a.ctypes.data)
+    b = np.empty(n, dtype=np.float64)
+    L.mpirg_gen_normal_matrix(n, 1, 0, b.ctypes.data)
+    return a, b
+
+
+def measured_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"), "/root/repo/MEASURED_PEAKS.json"):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return d, "measured"
+    return {"hbm_gbs": HBM_FALLBACK}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# Reference arm: the reference's CPU path (oracle/_ref), no GPU work.
+# ---------------------------------------------------------------------------
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    n = args.n
+    a, b = inputs(n)
+    impl = oracle.reference()
+    kind = "reference"
+    if impl is None:
+        impl, kind = oracle.restatement(), "port"
+    af = a.reshape(n, n).T  # column-major storage viewed as an (n, n) matrix
+    times = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        last = impl.ir(0, 1, 0, af, b, resid_term=False, ce=CE, litmax=LITMAX)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    sec = statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": sec, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32",
+        "data": "synthetic (seeded: Green's operator, libstdc++ mt19937_64 normal b)",
+        "config": {"workload": f"cfg2a: I-800G N={n}, <f64,f32,f64> LPS, ce={CE}, "
+                               f"litmax={LITMAX}", "n": n},
+        "cpu_baseline": {"value": sec, "unit": "s", "cores": 1, "kind": kind,
+                         "sample": f"full cfg2a solve (refactor + IR) at N={n}, "
+                                   "fp32 LU single-threaded per mp_structures.hpp:166-167"},
+        "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_split_s": {"factor": last["t_factor"], "solve": last["t_solve"]},
+        "iters": len(last["rhist"]) - 1, "reason": last["reason"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+def lu_work(n, nb):
+    """Algorithmic flops of the LU pieces (per factorization)."""
+    gemm = trsm = panel = 0.0
+    for k0 in range(0, n, nb):
+        jb = min(nb, n - k0)
+        m = n - k0
+        t = n - k0 - jb
+        gemm += 2.0 * t * t * jb
+        trsm += float(jb) * (jb - 1) * t
+        for j in range(jb):
+            panel += (m - j - 1) * (1 + 2 * (jb - j - 1))
+    return {"gemm": gemm, "trsm": trsm, "panel": panel, "total": 2.0 * n ** 3 / 3.0}
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+    from paper_2311_14616_b200 import _lib as L
+    lib = L.lib()
+    torch.cuda.set_device(local)
+    n = args.n
+    a_host, b_host = inputs(n)
+
+    cfg = L.mpirg_config(0, 1, 0, -1, 0, L.LU_EXACT, 0, local)
+    tp = L.mpirg_term_params(1.0, CE, 0.5, LITMAX)
+    a_dev = torch.from_numpy(a_host).cuda()
+    b_dev = torch.from_numpy(b_host).cuda()
+    sol_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    h = C.c_void_p()
+    err = L.mpirg_error()
+    L.check(lib.mpirg_factorization_create(C.byref(h), n, C.byref(cfg), a_dev.data_ptr(), 1,
+                                           C.byref(err)), err)
+    lib.mpirg_factorization_config(h, C.byref(cfg))
+    cap = LITMAX + 1
+    rh, dh = (C.c_double * cap)(), (C.c_double * cap)()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step(prof=False):
+        """One time-to-solution on resident data; returns (device ms, factor ms, report)."""
+        rep = L.mpirg_report(sol_dev.data_ptr(), 1, rh, dh, cap, 0, 0, 0, 0.0)
+        L.check(lib.mpirg_factorization_refactor(h, None, 1, C.byref(err)), err)
+        fms = lib.mpirg_factorization_last_factor_ms(h)
+        L.check(lib.mpirg_ir_solve(h, b_dev.data_ptr(), 1, C.byref(tp), C.byref(rep),
+                                   C.byref(err)), err)
+        return fms + rep.solve_ms, fms, rep
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # Timed region: K steps, L2 flushed between steps (flush excluded from the
+    # per-step CUDA-event times), per-kernel event timing on the handle's stream.
+    nclass = len(L.KERNEL_CLASSES)
+    ms_k = (C.c_double * nclass)()
+    cnt_k = (C.c_int * nclass)()
+    lib.mpirg_profile_collect(ms_k, cnt_k, nclass)
+    step_ms, fac_ms = [], []
+    rep = None
+    barrier(world)
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            lib.mpirg_profile_enable(1)
+            sms, fms, rep = step()
+            lib.mpirg_profile_enable(0)
+            step_ms.append(sms)
+            fac_ms.append(fms)
+        torch.cuda.synchronize()
+    barrier(world)
+    t_wall = time.perf_counter() - t_wall0
+    lib.mpirg_profile_collect(ms_k, cnt_k, nclass)
+    kernel_ms = {L.KERNEL_CLASSES[i]: ms_k[i] / args.steps for i in range(nclass)}
+    kernel_n = {L.KERNEL_CLASSES[i]: cnt_k[i] / args.steps for i in range(nclass)}
+    mean_ms = statistics.mean(step_ms)
+    mean_ms = max_over_ranks(mean_ms, world)
+    iters = rep.rhist_len - 1
+    reason = L.REASONS[rep.reason]
+
+    # e2e: public API with pinned host buffers (H2D of A,b and D2H of x timed).
+    e2e = None
+    if not args.no_e2e:
+        a_pin = torch.from_numpy(a_host).pin_memory()
+        b_pin = torch.from_numpy(b_host).pin_memory()
+        x_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+        e2e_t = []
+        for i in range(max(1, args.warmup // 2) + args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep2 = L.mpirg_report(x_pin.data_ptr(), 0, rh, dh, cap, 0, 0, 0, 0.0)
+            L.check(lib.mpirg_factorization_refactor(h, a_pin.data_ptr(), 0, C.byref(err)), err)
+            L.check(lib.mpirg_ir_solve(h, b_pin.data_ptr(), 0, C.byref(tp), C.byref(rep2),
+                                       C.byref(err)), err)
+            dt = time.perf_counter() - t0
+            if i >= max(1, args.warmup // 2):
+                e2e_t.append(dt)
+        e2e_s = max_over_ranks(statistics.mean(e2e_t), world)
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": n * n * 8 + n * 8,
+               "d2h_bytes_per_step": n * 8 + 3 * 8 * cap}
+
+    # Roofline of the dominant kernel class.
+    peaks, peak_src = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK))
+    ffma = C.c_double(0.0)
+    ffma_ms = C.c_double(0.0)
+    lib.mpirg_ffma_peak(C.byref(ffma), C.byref(ffma_ms))
+    nb = 64 if n <= 8192 else 32
+    work = lu_work(n, nb)
+    tf_b, tw_b = 4, 8
+    kernels = {}
+    for name in L.KERNEL_CLASSES:
+        kms = kernel_ms[name]
+        if kms <= 0:
+            continue
+        d = {"ms_per_step": kms, "launches_per_step": kernel_n[name],
+             "share_of_step": kms / mean_ms}
+        if name == "gemm":
+            d.update(bound="fp32-ffma", achieved=work["gemm"] / (kms * 1e-3) / 1e12,
+                     unit="TFLOP/s", peak=ffma.value)
+        elif name == "panel":
+            d.update(bound="latency (one pivot search per column)", unit="TFLOP/s",
+                     achieved=work["panel"] / (kms * 1e-3) / 1e12, peak=ffma.value)
+        elif name == "trsm":
+            d.update(bound="fp32-ffma", achieved=work["trsm"] / (kms * 1e-3) / 1e12,
+                     unit="TFLOP/s", peak=ffma.value)
+        elif name == "cast":
+            d.update(bound="hbm", achieved=n * n * (tw_b + tf_b) / (kms * 1e-3) / 1e9,
+                     unit="GB/s", peak=hbm)
+        elif name in ("trsv_lower", "trsv_upper"):
+            per = kernel_n[name]
+            d.update(bound="hbm", achieved=per * (n * n / 2.0) * tf_b / (kms * 1e-3) / 1e9,
+                     unit="GB/s", peak=hbm)
+        elif name == "residual":
+            per = kernel_n[name]
+            d.update(bound="hbm", achieved=per * n * n * tw_b / (kms * 1e-3) / 1e9,
+                     unit="GB/s", peak=hbm)
+        if "peak" in d and d["peak"]:
+            d["frac"] = d["achieved"] / d["peak"]
+        kernels[name] = d
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    dk = kernels[dom]
+    roof_bound = "hbm" if dk.get("bound") == "hbm" else "tensor"
+    roofline = {"kernel": dom, "bound": roof_bound, "bound_detail": dk.get("bound"),
+                "achieved": dk.get("achieved"), "peak": dk.get("peak"), "unit": dk.get("unit"),
+                "frac": dk.get("frac"), "traffic": None,
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if dk.get("unit") == "GB/s"
+                                else "fp32 FFMA microbenchmark (mpirg_ffma_peak) on this GPU; "
+                                     "TF32/tensor cores excluded by contract"),
+                "peak_kind": peak_src}
+    lu_ms = sum(kernel_ms[k] for k in ("panel", "moves", "trsm", "gemm"))
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(n, a_host, b_host)
+
+    if rank == 0:
+        launches = int(round(sum(kernel_n.values())))
+        line = {
+            "metric": METRIC, "value": mean_ms / 1e3, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64/f32 (TW=fp64, TF=fp32, TR=fp64)",
+            "data": "synthetic (seeded: Green's operator I-800G, libstdc++ mt19937_64 normal b)",
+            "config": {"workload": f"cfg2a: I-800G N={n}, <f64,f32,f64> LPS, ce={CE}, "
+                                   f"litmax={LITMAX}", "n": n, "nb": nb,
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "flushed between steps (256 MiB write), flush excluded",
+                       "a_resident_in_hbm": True},
+            "lu_gflops": work["total"] / (statistics.mean(fac_ms) * 1e-3) / 1e9,
+            "factor_ms": statistics.mean(fac_ms), "lu_kernels_ms": lu_ms,
+            "iters": iters, "reason": reason,
+            "roofline": roofline, "kernels": kernels,
+            "ffma_peak_tflops": ffma.value,
+            "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(), "wall_s_timed_region": t_wall,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    lib.mpirg_factorization_destroy(h)
+
+
+def cpu_baseline(n, a_host, b_host):
+    """The compiled reference (oracle/_ref) on this host: one full cfg2a solve."""
+    try:
+        import oracle
+        impl = oracle.reference()
+        kind = "reference"
+        if impl is None:
+            impl, kind = oracle.restatement(), "port"
+        af = a_host.reshape(n, n).T
+        t0 = time.perf_counter()
+        rep = impl.ir(0, 1, 0, af, b_host, resid_term=False, ce=CE, litmax=LITMAX)
+        dt = time.perf_counter() - t0
+        return {"value": dt, "unit": "s", "cores": 1, "kind": kind,
+                "sample": f"one full cfg2a solve (refactor + IR) at N={n}; fp32 LU is "
+                          "single-threaded in the reference (mp_structures.hpp:166-167)",
+                "iters": len(rep["rhist"]) - 1, "reason": rep["reason"]}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

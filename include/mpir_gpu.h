@@ -221,6 +221,29 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
                          mpirg_error *err);
 
 /* ---------------------------------------------------------------------------
+ * Measurement hooks (bench.py): per-kernel-class CUDA-event timing and an
+ * FP32 FFMA peak microbenchmark (the roofline denominator of the fp32 LU
+ * trailing update, which may not use tensor cores).
+ * ------------------------------------------------------------------------- */
+enum mpirg_kernel_class {
+  MPIRG_K_CAST = 0,       /* K1 cast + one-norm */
+  MPIRG_K_PANEL = 1,      /* K2 panel factorization (cluster) */
+  MPIRG_K_MOVES = 2,      /* K3 row moves (laswp gather) */
+  MPIRG_K_TRSM = 3,       /* K4 U12 = L11^-1 A12 */
+  MPIRG_K_GEMM = 4,       /* K5 trailing update */
+  MPIRG_K_TRSV_LOWER = 5, /* K6 forward substitution (+LPS/MPS prologue) */
+  MPIRG_K_TRSV_UPPER = 6, /* K6 back substitution (+IR epilogue) */
+  MPIRG_K_RESIDUAL = 7,   /* K7 compensated residual */
+  MPIRG_K_VECTOR = 8,     /* K8 small vector kernels */
+  MPIRG_K_COUNT = 9
+};
+void mpirg_profile_enable(int on);
+int mpirg_profile_collect(double *ms, int *count, int nclass);
+/* Runs a pure-FFMA kernel on the current device; *tflops = achieved fp32 FMA
+ * rate (2 flops per FFMA), *ms = its duration. */
+int mpirg_ffma_peak(double *tflops, double *ms);
+
+/* ---------------------------------------------------------------------------
  * Seeded input generators (host; not on the timed path). See problems.cpp.
  * ------------------------------------------------------------------------- */
 void mpirg_gen_uniform_matrix(int rows, int cols, uint64_t seed, double lo, double hi,

@@ -17,6 +17,8 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "mpir_gpu.h")
 
 B64, B32, B16 = 0, 1, 2
 LU_EXACT, LU_TC = 0, 1
+KERNEL_CLASSES = ["cast", "panel", "moves", "trsm", "gemm", "trsv_lower", "trsv_upper",
+                  "residual", "vector"]
 REASONS = ["SmallResidual", "SmallBackwardError", "ResidualStagnation",
            "CorrectionStagnation", "IterationLimit"]
 
@@ -133,6 +135,9 @@ PROTOTYPES = {
     "mpirg_batch_ir_solve": (_I, [_I, _I, C.POINTER(mpirg_config), _P, _P, _I,
                                   C.POINTER(mpirg_term_params), _P, _P, _P, _I, _P, _P, _P,
                                   C.POINTER(C.c_double), _E]),
+    "mpirg_profile_enable": (None, [_I]),
+    "mpirg_profile_collect": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_int), _I]),
+    "mpirg_ffma_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "mpirg_gen_uniform_matrix": (None, [_I, _I, C.c_uint64, _D, _D, _P]),
     "mpirg_gen_normal_matrix": (None, [_I, _I, C.c_uint64, _P]),
     "mpirg_gen_diag_dominant": (None, [_I, C.c_uint64, _D, _P]),

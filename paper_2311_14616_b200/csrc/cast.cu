@@ -192,6 +192,7 @@ void demote_t(const void *src, void *dst, size_t count, DevInfo *info, cudaStrea
   int grid = (int)std::min<size_t>((nvec + 255) / 256, 148 * 8);
   if (grid < 1)
     grid = 1;
+  ProfScope ps(KC_CAST, s);
   demote_kernel<From, To><<<grid, 256, 0, s>>>(static_cast<const From *>(src),
                                               static_cast<To *>(dst), count, info);
   MPIRG_CUDA_CHECK(cudaGetLastError());
@@ -205,6 +206,7 @@ void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long l
     return;
   const int stripes = (cols + 31) / 32;
   const int grid = (stripes + 3) / 4;
+  ProfScope ps(KC_CAST, s);
   cast_norm_kernel<From, To, NORM_ONLY><<<grid, 128, 0, s>>>(
       static_cast<const From *>(src), static_cast<To *>(dst), rows, cols, nb, info);
   MPIRG_CUDA_CHECK(cudaGetLastError());

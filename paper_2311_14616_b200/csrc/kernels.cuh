@@ -22,6 +22,30 @@ struct CudaError : std::runtime_error
   }
 };
 
+// ---- profiling hooks (prof.cu) --------------------------------------------
+enum KClass
+{
+  KC_CAST = 0,
+  KC_PANEL,
+  KC_MOVES,
+  KC_TRSM,
+  KC_GEMM,
+  KC_TRSV_L,
+  KC_TRSV_U,
+  KC_RESID,
+  KC_VEC
+};
+bool prof_on();
+void prof_begin(int kind, cudaStream_t s);
+void prof_end(int kind, cudaStream_t s);
+struct ProfScope
+{
+  int k;
+  cudaStream_t s;
+  ProfScope(int k_, cudaStream_t s_) : k(k_), s(s_) { prof_begin(k, s); }
+  ~ProfScope() { prof_end(k, s); }
+};
+
 // ---- K1: interprecision copy --------------------------------------------
 // Elementwise demotion (matrix.hpp:74-85 + precision.hpp:172-185), any length.
 void launch_demote(int from, int to, const void *src, void *dst, size_t count, DevInfo *info,

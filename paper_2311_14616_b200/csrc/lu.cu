@@ -568,6 +568,7 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
   PanelLaunch<T, NB>::configure();
   if (perm)
   {
+    ProfScope ps(KC_VEC, s);
     iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(perm, n);
     MPIRG_CUDA_CHECK(cudaGetLastError());
   }
@@ -594,16 +595,20 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    prof_begin(KC_PANEL, s);
     MPIRG_CUDA_CHECK(
         cudaLaunchKernelEx(&cfg, lu_panel_kernel<T, NB>, a, n, k0, jb, R, ipiv, mv, nm, info));
+    prof_end(KC_PANEL, s);
 
     const int ncols = n - jb;
     if (ncols > 0)
     {
       const int warps_needed = (ncols + 3) / 4;
       const int grid = std::max(1, std::min((warps_needed + 7) / 8, sms * 8));
+      prof_begin(KC_MOVES, s);
       lu_apply_moves_kernel<T, NB><<<grid, 256, 0, s>>>(a, n, k0, jb, mv, nm, perm);
       MPIRG_CUDA_CHECK(cudaGetLastError());
+      prof_end(KC_MOVES, s);
     }
     else if (perm)
     {
@@ -613,12 +618,16 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
     const int nt = n - k0 - jb;
     if (nt > 0)
     {
+      prof_begin(KC_TRSM, s);
       lu_trsm_kernel<T, NB><<<(nt + 127) / 128, 128, 0, s>>>(a, n, k0, jb);
       MPIRG_CUDA_CHECK(cudaGetLastError());
+      prof_end(KC_TRSM, s);
       const int tiles = (nt + GB - 1) / GB;
+      prof_begin(KC_GEMM, s);
       lu_gemm_kernel<T, NB><<<dim3(tiles, tiles), 256, gemm_smem_bytes<T, NB>(), s>>>(a, n, k0,
                                                                                      jb);
       MPIRG_CUDA_CHECK(cudaGetLastError());
+      prof_end(KC_GEMM, s);
     }
   }
 }

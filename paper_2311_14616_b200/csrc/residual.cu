@@ -226,6 +226,7 @@ void residual_t(const ResidualPlan &p, const void *x, const void *b, void *r,
 {
   const int n = p.n;
   const int grid = (n + 31) / 32;
+  ProfScope ps(KC_RESID, s);
   if (p.tmap)
   {
     constexpr int ST = 4;
@@ -333,6 +334,7 @@ void launch_ir_init(int tw, int tr, int n, const void *b, void *r, void *x,
                     unsigned long long *bnorm_bits, cudaStream_t s)
 {
   const int grid = std::min(148 * 4, (n + 255) / 256);
+  ProfScope ps(KC_VEC, s);
   if (tw == B64 && tr == B64)
     ir_init_kernel<double, double><<<grid, 256, 0, s>>>(n, (const double *)b, (double *)r,
                                                        (double *)x, bnorm_bits);
@@ -348,6 +350,7 @@ void launch_ir_init(int tw, int tr, int n, const void *b, void *r, void *x,
 void launch_ir_finish(int tw, int tr, int n, const void *x, void *sol, cudaStream_t s)
 {
   const int grid = std::min(148 * 4, (n + 255) / 256);
+  ProfScope ps(KC_VEC, s);
   if (tw == B64 && tr == B64)
     ir_finish_kernel<double, double><<<grid, 256, 0, s>>>(n, (const double *)x, (double *)sol);
   else if (tw == B32 && tr == B64)
