@@ -101,6 +101,13 @@ template <> __device__ __forceinline__ double zero_of<double>() { return 0.0; }
 template <> __device__ __forceinline__ float zero_of<float>() { return 0.0f; }
 template <> __device__ __forceinline__ h16 zero_of<h16>() { return h16{0}; }
 
+__device__ __forceinline__ double shfl_t(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ float shfl_t(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ h16 shfl_t(h16 v, int src)
+{
+  return h16{(uint16_t)__shfl_sync(0xffffffffu, (int)v.bits, src)};
+}
+
 // ---------------------------------------------------------------------------
 // NaN-propagating max of non-negative doubles via the IEEE bit order:
 // for x >= 0 (incl. +inf and positive NaN) the uint64 bit patterns are

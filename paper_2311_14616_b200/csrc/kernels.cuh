@@ -66,6 +66,8 @@ struct LuWorkspace
   int npanels = 0;
   int2 *moves = nullptr;  // [npanels][2*nb] (dst,src) row moves of each panel
   int *nmoves = nullptr;  // [npanels]
+  void *side = nullptr;   // cudaStream_t: look-ahead side stream
+  void *events = nullptr; // cudaEvent_t[3*npanels]
 };
 // Chooses the panel width for n and the factor precision (0 = auto).
 int lu_choose_nb(int prec, int n, int requested);

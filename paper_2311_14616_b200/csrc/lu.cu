@@ -13,19 +13,22 @@
 // first row (lowest index) maximising |a_ik| as a double, NaN never chosen,
 // and a NaN on the diagonal keeps p = k (dense_lu.hpp:65-78).
 //
-// Kernels per panel step (panel width nb, rows m = n - k0):
-//   lu_panel_kernel      one thread-block cluster (<= 16 CTAs, DSMEM) holds the
-//                        m x nb panel in shared memory; per column: local
-//                        argmax (warp shuffles), candidate rows broadcast into
-//                        every CTA's shared memory, one cluster barrier,
-//                        swap, scale (true division), rank-1 update.
-//                        Emits ipiv and the panel's row-move list.
-//   lu_apply_moves_kernel  applies the row moves (a permutation of <= 2nb rows)
-//                        as a gather to every column outside the panel and
-//                        to the accumulated permutation perm.
-//   lu_trsm_kernel       U12 = L11^{-1} A12, one thread per trailing column.
-//   lu_gemm_kernel       A22 -= L21 U12, SIMT register-tiled (fp32/fp64 FMA;
-//                        no TF32: that would change the factor precision).
+// Kernels per panel step p (panel width nb, k0 = p*nb, c0 = k0 + nb):
+//   lu_panel2_kernel     (lu_panel.cuh) one thread-block cluster factors the
+//                        (n-k0) x nb panel in registers; st.async/mbarrier
+//                        candidate exchange; emits ipiv + the row-move list.
+//   lu_mt_kernel         applies the panel's row moves (a permutation of
+//                        <= 2nb rows, as a gather) to trailing columns and
+//                        solves U12 = L11^{-1} A12 for them (k order).
+//   lu_gemm_kernel       A22 -= L21 U12, SIMT register-tiled FMA with the
+//                        accumulator initialised from A22, k ascending (no
+//                        TF32: that would change the factor precision).
+//   lu_apply_moves_kernel  the same row moves for the columns left of the
+//                        panel and for the accumulated permutation.
+// Schedule (look-ahead): the main stream runs the critical chain
+//   panel(p) -> mt(next nb columns) -> gemm(next nb columns) -> panel(p+1)
+// while a side stream applies mt + gemm to the remaining columns and the
+// left-column moves, overlapping the sequential panel chain.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -34,6 +37,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "lu_panel.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -43,255 +47,12 @@ namespace mpirg
 namespace
 {
 
-constexpr int PANEL_THREADS = 256;
-constexpr int PANEL_WARPS = PANEL_THREADS / 32;
-constexpr int MAX_CLUSTER = 16;
-
+// Gather-apply the panel's row moves (new[dst] = old[src]) to the columns
+// [cb, ce) -- one warp per column -- and to perm (block 0, warp 0).
 template <typename T, int NB>
-struct alignas(16) CandSlot
-{
-  T row[NB];
-  double val;
-  int idx;
-  int rowid;
-};
-
-template <typename T, int NB>
-struct alignas(16) RowKSlot
-{
-  T row[NB];
-  int rowid;
-  int nan;
-  int pad[2];
-};
-
-template <typename T, int NB>
-struct PanelShared
-{
-  CandSlot<T, NB> cand[2][MAX_CLUSTER];
-  RowKSlot<T, NB> rowk[2];
-  double redv[PANEL_WARPS];
-  int redi[PANEL_WARPS];
-};
-
-__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-
-template <typename T, int NB>
-__host__ __device__ constexpr size_t panel_smem_bytes(int R)
-{
-  return sizeof(PanelShared<T, NB>) + align16(sizeof(int) * (size_t)R) + sizeof(T) * (size_t)NB * R;
-}
-
-// (v1,i1) beats (v2,i2): larger |a|, ties to the lower row. Sentinel v = -1.
-__device__ __forceinline__ bool better(double v1, int i1, double v2, int i2)
-{
-  return v1 > v2 || (v1 == v2 && i1 < i2);
-}
-
-__device__ __forceinline__ bool isnan_t(double v) { return isnan(v); }
-__device__ __forceinline__ bool isnan_t(float v) { return isnan(v); }
-__device__ __forceinline__ bool isnan_t(h16 v) { return (v.bits & 0x7c00u) == 0x7c00u && (v.bits & 0x3ffu); }
-
-template <typename T, int NB>
-__global__ void __launch_bounds__(PANEL_THREADS, 1)
-    lu_panel_kernel(T *__restrict__ A, int n, int k0, int jb, int R, int *__restrict__ ipiv,
-                    int2 *__restrict__ moves, int *__restrict__ nmoves, DevInfo *info)
-{
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CS = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto &sh = *reinterpret_cast<PanelShared<T, NB> *>(smem_raw);
-  int *rowid = reinterpret_cast<int *>(smem_raw + sizeof(PanelShared<T, NB>));
-  T *P = reinterpret_cast<T *>(smem_raw + sizeof(PanelShared<T, NB>) + align16(sizeof(int) * R));
-
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int row0 = k0 + rank * R;
-  const int mloc = max(0, min(R, n - row0));
-
-  for (int c = 0; c < jb; ++c)
-  {
-    const T *col = A + (size_t)(k0 + c) * n + row0;
-    for (int i = t; i < mloc; i += PANEL_THREADS)
-      P[c * R + i] = col[i];
-  }
-  for (int i = t; i < mloc; i += PANEL_THREADS)
-    rowid[i] = row0 + i;
-  __syncthreads();
-
-  // Thread-local candidate for column 0 (rows g >= k0: all local rows).
-  double bv = -1.0;
-  int bi = INT_MAX;
-  for (int i = t; i < mloc; i += PANEL_THREADS)
-  {
-    const double a = fabs(to_d(P[i]));
-    if (!isnan(a) && better(a, row0 + i, bv, bi))
-    {
-      bv = a;
-      bi = row0 + i;
-    }
-  }
-
-  for (int j = 0; j < jb; ++j)
-  {
-    const int k = k0 + j;
-    const int par = j & 1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-    {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (better(ov, oi, bv, bi))
-      {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (lane == 0)
-    {
-      sh.redv[warp] = bv;
-      sh.redi[warp] = bi;
-    }
-    __syncthreads();
-    double cv = sh.redv[0];
-    int ci = sh.redi[0];
-#pragma unroll
-    for (int w = 1; w < PANEL_WARPS; ++w)
-      if (better(sh.redv[w], sh.redi[w], cv, ci))
-      {
-        cv = sh.redv[w];
-        ci = sh.redi[w];
-      }
-
-    // Broadcast this CTA's candidate row (full panel row) to every CTA.
-    const int cl = (ci != INT_MAX) ? ci - row0 : -1;
-    for (int q = t; q < CS * NB; q += PANEL_THREADS)
-    {
-      const int dst = q / NB, c = q % NB;
-      CandSlot<T, NB> *rs = cluster.map_shared_rank(&sh.cand[par][rank], dst);
-      rs->row[c] = (cl >= 0 && c < jb) ? P[c * R + cl] : T{};
-    }
-    if (t < CS)
-    {
-      CandSlot<T, NB> *rs = cluster.map_shared_rank(&sh.cand[par][rank], t);
-      rs->val = cv;
-      rs->idx = ci;
-      rs->rowid = cl >= 0 ? rowid[cl] : -1;
-    }
-    // The owner of row k broadcasts it too (the pivot row's new content).
-    const bool own_k = k >= row0 && k < row0 + mloc;
-    if (own_k)
-    {
-      const int kl = k - row0;
-      for (int q = t; q < CS * NB; q += PANEL_THREADS)
-      {
-        const int dst = q / NB, c = q % NB;
-        RowKSlot<T, NB> *rk = cluster.map_shared_rank(&sh.rowk[par], dst);
-        rk->row[c] = c < jb ? P[c * R + kl] : T{};
-      }
-      if (t < CS)
-      {
-        RowKSlot<T, NB> *rk = cluster.map_shared_rank(&sh.rowk[par], t);
-        rk->rowid = rowid[kl];
-        rk->nan = isnan_t(P[j * R + kl]) ? 1 : 0;
-      }
-    }
-    cluster.sync();
-
-    // Global decision, computed redundantly by every thread.
-    double gv = -1.0;
-    int gi = INT_MAX, gr = 0;
-    for (int r = 0; r < CS; ++r)
-    {
-      const double v = sh.cand[par][r].val;
-      const int i = sh.cand[par][r].idx;
-      if (better(v, i, gv, gi))
-      {
-        gv = v;
-        gi = i;
-        gr = r;
-      }
-    }
-    const bool knan = sh.rowk[par].nan != 0;
-    const int p = knan ? k : gi;
-    const T *U = knan ? sh.rowk[par].row : sh.cand[par][gr].row;
-    const T piv = U[j];
-    if (rank == 0 && t == 0)
-    {
-      ipiv[k] = p;
-      if (!knan && gv == 0.0)
-        atomicMin(&info->singular_col, k);
-    }
-    if (p != k)
-    {
-      if (p >= row0 && p < row0 + mloc)
-      {
-        const int pl = p - row0;
-        if (pl % PANEL_THREADS == t)
-        {
-          for (int c = 0; c < jb; ++c)
-            P[c * R + pl] = sh.rowk[par].row[c];
-          rowid[pl] = sh.rowk[par].rowid;
-        }
-      }
-      if (own_k)
-      {
-        const int kl = k - row0;
-        if (kl % PANEL_THREADS == t)
-        {
-          for (int c = 0; c < jb; ++c)
-            P[c * R + kl] = U[c];
-          rowid[kl] = sh.cand[par][gr].rowid;
-        }
-      }
-    }
-
-    // Scale (true division, dense_lu.hpp:87-89), rank-1 update of the rest of
-    // the panel (dense_lu.hpp:91-107), and the candidate for column j+1.
-    bv = -1.0;
-    bi = INT_MAX;
-    for (int i = t; i < mloc; i += PANEL_THREADS)
-    {
-      const int g = row0 + i;
-      if (g <= k)
-        continue;
-      const T l = divide(P[j * R + i], piv);
-      P[j * R + i] = l;
-      for (int c = j + 1; c < jb; ++c)
-        P[c * R + i] = upd(P[c * R + i], l, U[c]);
-      if (j + 1 < jb)
-      {
-        const double a = fabs(to_d(P[(j + 1) * R + i]));
-        if (!isnan(a) && better(a, g, bv, bi))
-        {
-          bv = a;
-          bi = g;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int c = 0; c < jb; ++c)
-  {
-    T *col = A + (size_t)(k0 + c) * n + row0;
-    for (int i = t; i < mloc; i += PANEL_THREADS)
-      col[i] = P[c * R + i];
-  }
-  for (int i = t; i < mloc; i += PANEL_THREADS)
-    if (rowid[i] != row0 + i)
-    {
-      const int q = atomicAdd(nmoves, 1);
-      moves[q] = make_int2(row0 + i, rowid[i]);
-    }
-  // No CTA may exit while others can still touch its shared memory.
-  cluster.sync();
-}
-
-// Gather-apply the panel's row moves (new[dst] = old[src]) to columns
-// [0, k0) and [k0+jb, n) -- one warp per column -- and to perm (block 0).
-template <typename T, int NB>
-__global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, int n, int k0,
-                                                             int jb, const int2 *__restrict__ moves,
+__global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, int n, int cb,
+                                                             int ce,
+                                                             const int2 *__restrict__ moves,
                                                              const int *__restrict__ nmoves,
                                                              int *__restrict__ perm)
 {
@@ -307,7 +68,7 @@ __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, 
     const int e = lane + 32 * q;
     mv[q] = e < nm ? moves[e] : make_int2(-1, -1);
   }
-  const int ncols = n - jb;
+  const int ncols = ce - cb;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   if (blockIdx.x == 0 && threadIdx.x < 32 && perm)
@@ -329,70 +90,151 @@ __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, 
     T v[UNR][PER];
 #pragma unroll
     for (int u = 0; u < UNR; ++u)
-    {
-      const int cc = c0 + u;
-      if (cc < ncols)
+      if (c0 + u < ncols)
       {
-        const int col = cc < k0 ? cc : cc + jb;
-        const T *cp = A + (size_t)col * n;
+        const T *cp = A + (size_t)(cb + c0 + u) * n;
 #pragma unroll
         for (int q = 0; q < PER; ++q)
           if (mv[q].x >= 0)
             v[u][q] = cp[mv[q].y];
       }
-    }
     __syncwarp();
 #pragma unroll
     for (int u = 0; u < UNR; ++u)
-    {
-      const int cc = c0 + u;
-      if (cc < ncols)
+      if (c0 + u < ncols)
       {
-        const int col = cc < k0 ? cc : cc + jb;
-        T *cp = A + (size_t)col * n;
+        T *cp = A + (size_t)(cb + c0 + u) * n;
 #pragma unroll
         for (int q = 0; q < PER; ++q)
           if (mv[q].x >= 0)
             cp[mv[q].x] = v[u][q];
       }
-    }
   }
 }
 
-// U12 = L11^{-1} A12 (unit lower), one thread per trailing column, k order.
+// Row moves + U12 = L11^{-1} A12 for the trailing columns [cb, ce).
+// CTA = 4 warps, 32 columns (8 per warp). Phase 1: each warp gathers the
+// moves of its 8 columns (lanes over move entries). Phase 2: each warp solves
+// its 8 columns at once -- lane owns panel rows (lane, lane+32), x_k is
+// broadcast by shuffle, k ascending, one update per element per step, so the
+// per-element chain is the reference's (dense_lu.hpp:91-107 restricted to
+// the panel rows).
+constexpr int MT_COLS = 32;
 template <typename T, int NB>
-__global__ void __launch_bounds__(128) lu_trsm_kernel(T *__restrict__ A, int n, int k0, int jb)
+__global__ void __launch_bounds__(128) lu_mt_kernel(T *__restrict__ A, int n, int k0, int jb,
+                                                    int cb, int ce,
+                                                    const int2 *__restrict__ moves,
+                                                    const int *__restrict__ nmoves)
 {
+  constexpr int PER = (2 * NB + 31) / 32;
+  constexpr int RL = (NB + 31) / 32;  // panel rows per lane
   __shared__ T L[NB][NB + 1];
-  for (int idx = threadIdx.x; idx < jb * jb; idx += blockDim.x)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   {
-    const int kk = idx / jb, i = idx % jb;
-    L[i][kk] = A[(size_t)(k0 + kk) * n + k0 + i];
+    // stage L11 with all loads in flight before the stores
+    constexpr int PT = (NB * NB + 127) / 128;
+    T tmp[PT];
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int idx = threadIdx.x + u * 128;
+      const int kk = idx / NB, i = idx % NB;
+      tmp[u] = (kk < jb && i < jb) ? A[(size_t)(k0 + kk) * n + k0 + i] : T{};
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int idx = threadIdx.x + u * 128;
+      const int kk = idx / NB, i = idx % NB;
+      if (kk < NB)
+        L[i][kk] = tmp[u];
+    }
   }
-  __syncthreads();
-  const int col = k0 + jb + blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= n)
-    return;
-  T *cp = A + (size_t)col * n + k0;
-  T x[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i)
-    if (i < jb)
-      x[i] = cp[i];
-#pragma unroll
-  for (int kk = 0; kk < NB; ++kk)
+  const int nm = *nmoves;
+  const int col0 = cb + blockIdx.x * MT_COLS + warp * 8;
+  // phase 1: gather the row moves for this warp's 8 columns
+  if (nm > 0)
   {
-    if (kk >= jb)
-      break;
+    int2 mv[PER];
 #pragma unroll
-    for (int i = kk + 1; i < NB; ++i)
-      if (i < jb)
-        x[i] = upd(x[i], L[i][kk], x[kk]);
+    for (int q = 0; q < PER; ++q)
+    {
+      const int e = lane + 32 * q;
+      mv[q] = e < nm ? moves[e] : make_int2(-1, -1);
+    }
+    T v[8][PER];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (col0 + u < ce)
+      {
+        const T *cp = A + (size_t)(col0 + u) * n;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            v[u][q] = cp[mv[q].y];
+      }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (col0 + u < ce)
+      {
+        T *cp = A + (size_t)(col0 + u) * n;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            cp[mv[q].x] = v[u][q];
+      }
+    __syncwarp();
+  }
+  __syncthreads();  // L staged; this warp's gathered values visible to itself
+  // phase 2: forward substitution on the panel rows of 8 columns
+  T x[8][RL];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      x[u][h] = (col0 + u < ce && i < jb) ? A[(size_t)(col0 + u) * n + k0 + i] : T{};
+    }
+#pragma unroll 1
+  for (int kk = 0; kk < jb; ++kk)
+  {
+    const int hk = kk >> 5, lk = kk & 31;
+    T lv[RL];
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      lv[h] = (i > kk && i < jb) ? L[i][kk] : T{};
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+    {
+      T src = x[u][0];
+#pragma unroll
+      for (int h = 1; h < RL; ++h)
+        if (hk == h)
+          src = x[u][h];
+      const T xk = shfl_t(src, lk);
+#pragma unroll
+      for (int h = 0; h < RL; ++h)
+      {
+        const int i = lane + 32 * h;
+        if (i > kk && i < jb)
+          x[u][h] = upd(x[u][h], lv[h], xk);
+      }
+    }
   }
 #pragma unroll
-  for (int i = 0; i < NB; ++i)
-    if (i < jb)
-      cp[i] = x[i];
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      if (col0 + u < ce && i < jb)
+        A[(size_t)(col0 + u) * n + k0 + i] = x[u][h];
+    }
 }
 
 // ---- trailing update A22 -= L21 * U12 ------------------------------------
@@ -430,8 +272,10 @@ constexpr size_t gemm_smem_bytes()
   return sizeof(C) * (size_t)NB * GB + sizeof(C) * (size_t)NB * (GB + GPAD);
 }
 
+// C = A[r0.., cb..ce) for rows >= c0; L21 = A[rows, k0..k0+jb); U12 = A[k0.., cols].
 template <typename T, int NB>
-__global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, int k0, int jb)
+__global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, int k0, int jb,
+                                                      int cb, int ce)
 {
   using C = typename CType<T>::type;
   extern __shared__ __align__(16) unsigned char gsm[];
@@ -439,21 +283,31 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
   C *Bs = As + (size_t)NB * GB;                        // [NB][GB+GPAD]
   const int c0 = k0 + jb;
   const int r0 = c0 + blockIdx.x * GB;
-  const int cc0 = c0 + blockIdx.y * GB;
+  const int cc0 = cb + blockIdx.y * GB;
   const int t = threadIdx.x;
   const int tx = t & 15, ty = t >> 4;
 
-  for (int idx = t; idx < jb * GB; idx += 256)
   {
-    const int kk = idx / GB, m = idx % GB;
-    const int row = r0 + m;
-    As[kk * GB + m] = row < n ? to_c(A[(size_t)(k0 + kk) * n + row]) : C(0);
-  }
-  for (int idx = t; idx < jb * GB; idx += 256)
-  {
-    const int nn = idx / jb, kk = idx % jb;
-    const int col = cc0 + nn;
-    Bs[kk * (GB + GPAD) + nn] = col < n ? to_c(A[(size_t)col * n + k0 + kk]) : C(0);
+    constexpr int PT = NB * GB / 256;  // elements per thread per operand
+    C ta[PT], tb[PT];
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int idx = t + u * 256;
+      const int kk = idx / GB, m = idx % GB;
+      const int row = r0 + m;
+      ta[u] = (kk < jb && row < n) ? to_c(A[(size_t)(k0 + kk) * n + row]) : C(0);
+      const int nn = idx / NB, kb = idx % NB;
+      const int col = cc0 + nn;
+      tb[u] = (kb < jb && col < ce) ? to_c(A[(size_t)col * n + k0 + kb]) : C(0);
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int idx = t + u * 256;
+      As[(idx / GB) * GB + idx % GB] = ta[u];
+      Bs[(idx % NB) * (GB + GPAD) + idx / NB] = tb[u];
+    }
   }
 
   C acc[8][8];
@@ -465,7 +319,7 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
     for (int i = 0; i < 8; ++i)
     {
       const int row = r0 + (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
-      acc[i][j] = (row < n && col < n) ? to_c(A[(size_t)col * n + row]) : C(0);
+      acc[i][j] = (row < n && col < ce) ? to_c(A[(size_t)col * n + row]) : C(0);
     }
   }
   __syncthreads();
@@ -498,7 +352,7 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
     for (int i = 0; i < 8; ++i)
     {
       const int row = r0 + (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
-      if (row < n && col < n)
+      if (row < n && col < ce)
         from_c(A[(size_t)col * n + row], acc[i][j]);
     }
   }
@@ -512,7 +366,7 @@ __global__ void iota_kernel(int *p, int n)
 
 __global__ void perm_from_ipiv_kernel(const int *__restrict__ ipiv, int n, int *__restrict__ perm)
 {
-  // Sequential by construction (apply_pivots order); n is small on this path.
+  // Sequential by construction (apply_pivots order); used only off the hot path.
   if (threadIdx.x != 0)
     return;
   for (int i = 0; i < n; ++i)
@@ -530,119 +384,188 @@ __global__ void perm_from_ipiv_kernel(const int *__restrict__ ipiv, int n, int *
 }
 
 // ---- host orchestration --------------------------------------------------
-template <typename T, int NB>
-struct PanelLaunch
+template <typename T, int NB, int RPT>
+void configure_panel()
 {
-  static bool configured;
-  static void configure()
-  {
-    if (configured)
-      return;
-    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_kernel<T, NB>,
-                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_kernel<T, NB>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          220 * 1024));
-    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_kernel<T, NB>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)gemm_smem_bytes<T, NB>()));
-    configured = true;
-  }
-};
-template <typename T, int NB>
-bool PanelLaunch<T, NB>::configured = false;
+  static bool done = false;
+  if (done)
+    return;
+  MPIRG_CUDA_CHECK(cudaFuncSetAttribute(panel2::lu_panel2_kernel<T, NB, RPT>,
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  MPIRG_CUDA_CHECK(cudaFuncSetAttribute(panel2::lu_panel2_kernel<T, NB, RPT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)panel2::panel_dyn_smem<T, NB, RPT>()));
+  done = true;
+}
 
 template <typename T, int NB>
-void panel_geometry(int m, int &cs, int &R)
+void configure_gemm()
 {
-  cs = std::min(MAX_CLUSTER, std::max(1, (m + PANEL_THREADS - 1) / PANEL_THREADS));
-  R = (m + cs - 1) / cs;
-  while (panel_smem_bytes<T, NB>(R) > 220 * 1024)
-    throw std::runtime_error("LU panel does not fit in a 16-CTA cluster at this n; use a "
-                             "smaller nb");
+  static bool done = false;
+  if (done)
+    return;
+  MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_kernel<T, NB>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)gemm_smem_bytes<T, NB>()));
+  done = true;
+}
+
+template <typename T, int NB, int RPT>
+void launch_panel_rpt(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm,
+                      DevInfo *info, cudaStream_t s)
+{
+  configure_panel<T, NB, RPT>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(panel2::NT);
+  cfg.dynamicSmemBytes = panel2::panel_dyn_smem<T, NB, RPT>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT>, a, n, k0, jb,
+                                      ipiv, mv, nm, info));
+}
+
+// Largest rows-per-thread the register file allows for (T, NB).
+template <typename T, int NB>
+constexpr int max_rpt()
+{
+  return panel2::panel_dyn_smem<T, NB, 4>() <= 180 * 1024
+             ? 4
+             : (panel2::panel_dyn_smem<T, NB, 2>() <= 180 * 1024 ? 2 : 1);
+}
+
+template <typename T, int NB>
+void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, DevInfo *info,
+                  cudaStream_t s)
+{
+  const int m = n - k0;
+  const int per_cta = panel2::NT;
+  int rpt = 1;
+  while (rpt * per_cta * panel2::MAXCS < m)
+    rpt *= 2;
+  if (rpt > max_rpt<T, NB>())
+    throw std::runtime_error("LU panel: n too large for a single-cluster panel at this nb");
+  const int cs = std::max(1, (m + rpt * per_cta - 1) / (rpt * per_cta));
+  prof_begin(KC_PANEL, s);
+  if (rpt == 1)
+    launch_panel_rpt<T, NB, 1>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  else if (rpt == 2)
+  {
+    if constexpr (max_rpt<T, NB>() >= 2)
+      launch_panel_rpt<T, NB, 2>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  }
+  else
+  {
+    if constexpr (max_rpt<T, NB>() >= 4)
+      launch_panel_rpt<T, NB, 4>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  }
+  prof_end(KC_PANEL, s);
+}
+
+template <typename T, int NB>
+void launch_mt(T *a, int n, int k0, int jb, int cb, int ce, const int2 *mv, const int *nm,
+               cudaStream_t s)
+{
+  if (ce <= cb)
+    return;
+  prof_begin(KC_TRSM, s);
+  lu_mt_kernel<T, NB><<<(ce - cb + MT_COLS - 1) / MT_COLS, 128, 0, s>>>(a, n, k0, jb, cb, ce, mv,
+                                                                      nm);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+  prof_end(KC_TRSM, s);
+}
+
+template <typename T, int NB>
+void launch_gemm(T *a, int n, int k0, int jb, int cb, int ce, cudaStream_t s)
+{
+  const int c0 = k0 + jb;
+  if (ce <= cb || c0 >= n)
+    return;
+  configure_gemm<T, NB>();
+  prof_begin(KC_GEMM, s);
+  const dim3 grid((n - c0 + GB - 1) / GB, (ce - cb + GB - 1) / GB);
+  lu_gemm_kernel<T, NB><<<grid, 256, gemm_smem_bytes<T, NB>(), s>>>(a, n, k0, jb, cb, ce);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+  prof_end(KC_GEMM, s);
+}
+
+template <typename T, int NB>
+void launch_moves(T *a, int n, int cb, int ce, const int2 *mv, const int *nm, int *perm,
+                  cudaStream_t s)
+{
+  const int ncols = ce - cb;
+  if (ncols <= 0 && !perm)
+    return;
+  prof_begin(KC_MOVES, s);
+  const int warps_needed = std::max(1, (ncols + 3) / 4);
+  const int grid = std::max(1, std::min((warps_needed + 7) / 8, 148 * 8));
+  lu_apply_moves_kernel<T, NB><<<grid, 256, 0, s>>>(a, n, cb, std::max(cb, ce), mv, nm, perm);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+  prof_end(KC_MOVES, s);
 }
 
 template <typename T, int NB>
 void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, cudaStream_t s)
 {
-  PanelLaunch<T, NB>::configure();
+  cudaStream_t side = static_cast<cudaStream_t>(ws.side);
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);  // [3][npanels]: P, N, R
+  const int np = ws.npanels;
   if (perm)
   {
     ProfScope ps(KC_VEC, s);
     iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(perm, n);
     MPIRG_CUDA_CHECK(cudaGetLastError());
   }
-  MPIRG_CUDA_CHECK(cudaMemsetAsync(ws.nmoves, 0, sizeof(int) * ws.npanels, s));
-  int sms = 148;
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(ws.nmoves, 0, sizeof(int) * np, s));
+  MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, ev[0], 0));
   for (int p = 0, k0 = 0; k0 < n; ++p, k0 += NB)
   {
     const int jb = std::min(NB, n - k0);
-    const int m = n - k0;
-    int cs, R;
-    panel_geometry<T, NB>(m, cs, R);
+    const int c0 = k0 + jb;
     int2 *mv = ws.moves + (size_t)p * 2 * NB;
     int *nm = ws.nmoves + p;
-
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(PANEL_THREADS);
-    cfg.dynamicSmemBytes = panel_smem_bytes<T, NB>(R);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    prof_begin(KC_PANEL, s);
-    MPIRG_CUDA_CHECK(
-        cudaLaunchKernelEx(&cfg, lu_panel_kernel<T, NB>, a, n, k0, jb, R, ipiv, mv, nm, info));
-    prof_end(KC_PANEL, s);
-
-    const int ncols = n - jb;
-    if (ncols > 0)
+    cudaEvent_t evP = ev[p], evN = ev[np + p], evR = ev[2 * np + p];
+    // main: the critical chain
+    launch_panel<T, NB>(a, n, k0, jb, ipiv, mv, nm, info, s);
+    MPIRG_CUDA_CHECK(cudaEventRecord(evP, s));
+    const int cnext = std::min(n, c0 + NB);
+    if (c0 < n)
     {
-      const int warps_needed = (ncols + 3) / 4;
-      const int grid = std::max(1, std::min((warps_needed + 7) / 8, sms * 8));
-      prof_begin(KC_MOVES, s);
-      lu_apply_moves_kernel<T, NB><<<grid, 256, 0, s>>>(a, n, k0, jb, mv, nm, perm);
-      MPIRG_CUDA_CHECK(cudaGetLastError());
-      prof_end(KC_MOVES, s);
+      if (p > 0)
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + p - 1], 0));
+      launch_mt<T, NB>(a, n, k0, jb, c0, cnext, mv, nm, s);
+      launch_gemm<T, NB>(a, n, k0, jb, c0, cnext, s);
     }
-    else if (perm)
+    MPIRG_CUDA_CHECK(cudaEventRecord(evN, s));
+    // side: the rest of this step's update + the left-column moves
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, evP, 0));
+    if (cnext < n)
     {
-      lu_apply_moves_kernel<T, NB><<<1, 32, 0, s>>>(a, n, k0, jb, mv, nm, perm);
-      MPIRG_CUDA_CHECK(cudaGetLastError());
+      launch_mt<T, NB>(a, n, k0, jb, cnext, n, mv, nm, side);
+      launch_gemm<T, NB>(a, n, k0, jb, cnext, n, side);
     }
-    const int nt = n - k0 - jb;
-    if (nt > 0)
-    {
-      prof_begin(KC_TRSM, s);
-      lu_trsm_kernel<T, NB><<<(nt + 127) / 128, 128, 0, s>>>(a, n, k0, jb);
-      MPIRG_CUDA_CHECK(cudaGetLastError());
-      prof_end(KC_TRSM, s);
-      const int tiles = (nt + GB - 1) / GB;
-      prof_begin(KC_GEMM, s);
-      lu_gemm_kernel<T, NB><<<dim3(tiles, tiles), 256, gemm_smem_bytes<T, NB>(), s>>>(a, n, k0,
-                                                                                     jb);
-      MPIRG_CUDA_CHECK(cudaGetLastError());
-      prof_end(KC_GEMM, s);
-    }
+    launch_moves<T, NB>(a, n, 0, k0, mv, nm, perm, side);
+    MPIRG_CUDA_CHECK(cudaEventRecord(evR, side));
   }
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + np - 1], 0));
 }
 
 }  // namespace
 
 int lu_choose_nb(int prec, int n, int requested)
 {
-  if (requested == 32 || requested == 64)
+  if (requested == 16 || requested == 32 || requested == 64)
     return requested;
   if (prec == B64)
-    return 32;
-  if (prec == B32)
-    return n <= 8192 ? 64 : 32;
-  return 64;
+    return n <= 4096 ? 64 : (n <= 8192 ? 32 : 16);
+  return n <= 8192 ? 64 : 32;
 }
 
 void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
@@ -650,9 +573,16 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   lu_workspace_free(ws);
   ws.n = n;
   ws.nb = lu_choose_nb(prec, n, nb);
-  ws.npanels = (n + ws.nb - 1) / ws.nb;
+  ws.npanels = std::max(1, (n + ws.nb - 1) / ws.nb);
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.moves, sizeof(int2) * (size_t)ws.npanels * 2 * ws.nb));
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.nmoves, sizeof(int) * (size_t)ws.npanels));
+  cudaStream_t side;
+  MPIRG_CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  ws.side = side;
+  auto *ev = new cudaEvent_t[3 * (size_t)ws.npanels];
+  for (int i = 0; i < 3 * ws.npanels; ++i)
+    MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  ws.events = ev;
 }
 
 void lu_workspace_free(LuWorkspace &ws)
@@ -661,7 +591,28 @@ void lu_workspace_free(LuWorkspace &ws)
     cudaFree(ws.moves);
   if (ws.nmoves)
     cudaFree(ws.nmoves);
+  if (ws.events)
+  {
+    auto *ev = static_cast<cudaEvent_t *>(ws.events);
+    for (int i = 0; i < 3 * ws.npanels; ++i)
+      cudaEventDestroy(ev[i]);
+    delete[] ev;
+  }
+  if (ws.side)
+    cudaStreamDestroy(static_cast<cudaStream_t>(ws.side));
   ws = LuWorkspace{};
+}
+
+template <typename T>
+void lu_dispatch(int nb, T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                 cudaStream_t s)
+{
+  if (nb == 64)
+    lu_run<T, 64>(a, n, ipiv, perm, ws, info, s);
+  else if (nb == 32)
+    lu_run<T, 32>(a, n, ipiv, perm, ws, info, s);
+  else
+    lu_run<T, 16>(a, n, ipiv, perm, ws, info, s);
 }
 
 void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWorkspace &ws,
@@ -671,26 +622,11 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
     return;
   (void)lu_mode;
   if (prec == B64)
-  {
-    if (ws.nb == 64)
-      lu_run<double, 64>(static_cast<double *>(a), n, ipiv, perm, ws, info, s);
-    else
-      lu_run<double, 32>(static_cast<double *>(a), n, ipiv, perm, ws, info, s);
-  }
+    lu_dispatch<double>(ws.nb, static_cast<double *>(a), n, ipiv, perm, ws, info, s);
   else if (prec == B32)
-  {
-    if (ws.nb == 64)
-      lu_run<float, 64>(static_cast<float *>(a), n, ipiv, perm, ws, info, s);
-    else
-      lu_run<float, 32>(static_cast<float *>(a), n, ipiv, perm, ws, info, s);
-  }
+    lu_dispatch<float>(ws.nb, static_cast<float *>(a), n, ipiv, perm, ws, info, s);
   else
-  {
-    if (ws.nb == 64)
-      lu_run<h16, 64>(static_cast<h16 *>(a), n, ipiv, perm, ws, info, s);
-    else
-      lu_run<h16, 32>(static_cast<h16 *>(a), n, ipiv, perm, ws, info, s);
-  }
+    lu_dispatch<h16>(ws.nb, static_cast<h16 *>(a), n, ipiv, perm, ws, info, s);
 }
 
 void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s)
