@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -446,8 +447,13 @@ void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, Dev
 {
   const int m = n - k0;
   const int per_cta = panel2::NT;
+  static const int max_cs = [] {
+    const char *e = std::getenv("MPIRG_PANEL_MAXCS");
+    const int v = e ? std::atoi(e) : panel2::MAXCS;
+    return std::max(1, std::min(panel2::MAXCS, v));
+  }();
   int rpt = 1;
-  while (rpt * per_cta * panel2::MAXCS < m)
+  while (rpt * per_cta * max_cs < m)
     rpt *= 2;
   if (rpt > max_rpt<T, NB>())
     throw std::runtime_error("LU panel: n too large for a single-cluster panel at this nb");

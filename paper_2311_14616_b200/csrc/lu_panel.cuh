@@ -44,23 +44,33 @@ constexpr int IB = 8;
 template <typename T, int NB>
 struct alignas(16) Slot
 {
-  double val;  // |pivot candidate| as double, -1 = none
-  int pos;     // its current position (INT_MAX = none)
-  int nan;     // the row at position k holds a NaN in column k
-  T row[NB];   // the candidate row (panel columns, as of this step)
+  unsigned long long key;  // mag_key of the candidate, 0 = none
+  int pos;                 // its current position (INT_MAX = none)
+  int nan;                 // the row at position k holds a NaN in column k
+  T row[NB];               // the candidate row (panel columns, as of this step)
 };
 
 // Warp-level candidate staged for the CTA reduction.
 template <typename T>
 struct alignas(16) WSlot
 {
-  double val;
+  unsigned long long key;
   int pos;
   int nan;
   int lrow;  // local row index (for the columns right of the block, in P)
   int pad[3];
   T blk[IB];  // the block columns (registers of the owner thread)
 };
+
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cluster, uint32_t src_cta,
+                                               uint32_t bytes, uint32_t bar_cluster)
+{
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];" ::"r"(dst_cluster),
+      "r"(src_cta), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
 
 __device__ __forceinline__ bool better(double v1, int p1, double v2, int p2)
 {
@@ -86,6 +96,47 @@ __device__ __forceinline__ unsigned long long cand_bits(double a)
 {
   // +0.0 and positive values map above 0 so "no candidate" can be 0.
   return (unsigned long long)__double_as_longlong(a) + 1ull;
+}
+
+// Candidate key of |a| (a non-NaN): its IEEE bits + 1, so 0 means "none" and
+// the unsigned order is the numeric order of the (non-negative) magnitudes.
+__device__ __forceinline__ unsigned long long mag_key(float a)
+{
+  return (unsigned long long)__float_as_uint(fabsf(a)) + 1ull;
+}
+__device__ __forceinline__ unsigned long long mag_key(double a)
+{
+  return (unsigned long long)__double_as_longlong(fabs(a)) + 1ull;
+}
+__device__ __forceinline__ unsigned long long mag_key(h16 a) { return mag_key(h2f(a)); }
+__device__ __forceinline__ bool is_nan_t(float a) { return isnan(a); }
+__device__ __forceinline__ bool is_nan_t(double a) { return isnan(a); }
+__device__ __forceinline__ bool is_nan_t(h16 a) { return (a.bits & 0x7c00u) == 0x7c00u && (a.bits & 0x3ffu); }
+
+// Warp-uniform argmax over (key, pos): the largest key, ties to the lowest
+// position. redux.sync does each reduction in one instruction; 64-bit keys
+// (binary64 magnitudes) take a hi/lo pass.
+template <bool WIDE>
+__device__ __forceinline__ void argmax_redux(unsigned long long key, int pos,
+                                             unsigned long long &mkey, int &mpos)
+{
+  if constexpr (!WIDE)
+  {
+    const unsigned k32 = (unsigned)key;
+    const unsigned m = __reduce_max_sync(0xffffffffu, k32);
+    mkey = m;
+    mpos = (int)__reduce_min_sync(0xffffffffu, (k32 == m && m != 0u) ? (unsigned)pos
+                                                                      : 0x7fffffffu);
+  }
+  else
+  {
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    mkey = ((unsigned long long)mh << 32) | ml;
+    mpos = (int)__reduce_min_sync(0xffffffffu, (key == mkey && mkey != 0ull) ? (unsigned)pos
+                                                                           : 0x7fffffffu);
+  }
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p)
@@ -127,7 +178,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
       "{\n"
       ".reg .pred p;\n"
       "W_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra W_%=;\n"
       "}\n" ::"r"(smem_addr(bar)),
       "r"(phase)
@@ -164,6 +215,24 @@ __host__ __device__ constexpr size_t panel_dyn_smem()
   return a16(sizeof(T) * (size_t)NB * RPT * NT) + a16(sizeof(T) * (size_t)IB * NB);
 }
 
+#ifdef MPIRG_DEBUG_PANEL
+#define PT_MARK(i)                                                         \
+  do                                                                       \
+  {                                                                        \
+    if (t == 0)                                                            \
+    {                                                                      \
+      const long long now = clock64();                                     \
+      ptacc[i] += now - ptlast;                                            \
+      ptlast = now;                                                        \
+    }                                                                      \
+  } while (0)
+#else
+#define PT_MARK(i) \
+  do                \
+  {                 \
+  } while (0)
+#endif
+
 // rows of this CTA: row0 + t + q*NT, q < RPT (R = RPT*NT rows per CTA)
 template <typename T, int NB, int RPT>
 __global__ void __launch_bounds__(NT, 1)
@@ -171,15 +240,16 @@ __global__ void __launch_bounds__(NT, 1)
                      int2 *__restrict__ moves, int *__restrict__ nmoves, DevInfo *info)
 {
   using S = Slot<T, NB>;
-  constexpr int NCH = sizeof(S) / 16;
   constexpr int R = RPT * NT;
+  constexpr bool WIDE = sizeof(T) > 4;
   static_assert(sizeof(S) % 16 == 0, "slot must be a multiple of 16 bytes");
   static_assert(NB % IB == 0, "NB must be a multiple of IB");
-  __shared__ WSlot<T> wslot[2][NW];  // double-buffered: a slow pusher of step j never sees step j+1
-  __shared__ S inbox[2][MAXCS];
+  __shared__ WSlot<T> wslot[2][NW];  // double-buffered: a slow reader of step j never sees j+1
+  __shared__ S sendbuf[2];           // this CTA's candidate, assembled for the bulk push
+  __shared__ S inbox[2][MAXCS];      // every CTA's candidate (filled by bulk copies)
   __shared__ __align__(8) uint64_t bars[2];
   extern __shared__ __align__(16) unsigned char dsm[];
-  T *P = reinterpret_cast<T *>(dsm);                                   // [NB][R]
+  T *P = reinterpret_cast<T *>(dsm);                                     // [NB][R]
   T *Ub = reinterpret_cast<T *>(dsm + a16(sizeof(T) * (size_t)NB * R));  // [IB][NB]
 
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -211,52 +281,50 @@ __global__ void __launch_bounds__(NT, 1)
         if (c0 + u < NB)
           P[(c0 + u) * R + t + q * NT] = tmp[u][q];
   }
-  // Bytes my inbox receives at step s (all CS candidates; chunks left of the
-  // step's block are not sent).
+  const bool multi = CS > 1;
+  // Bytes my inbox receives at step s: the header and the chunks from the
+  // step's block start on, from each of the CS CTAs.
   auto step_bytes = [&](int s) -> uint32_t {
     const int blk0 = (s / IB) * IB;
-    return (uint32_t)(CS * (NCH - (int)((blk0 * sizeof(T)) / 16)) * 16);
+    return (uint32_t)(CS * ((int)(sizeof(S) / 16) - (int)((blk0 * sizeof(T)) / 16)) * 16);
   };
-  if (t == 0)
+  if (t == 0 && multi)
   {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // Arm the first two phases before any peer can send (the expect_tx must
-    // precede every complete_tx of its phase).
+    // Arm the first two phases before any peer can send.
     mbar_expect_tx(&bars[0], step_bytes(0));
     if (jb > 1)
       mbar_expect_tx(&bars[1], step_bytes(1));
   }
-  cluster_sync_all();
+  if (multi)
+    cluster_sync_all();
+  else
+    __syncthreads();
 
-  // Push assignment (fixed for the whole panel): chunk idx = t + u*NT of the
-  // CS*NCH chunks goes to CTA idx / NCH, chunk idx % NCH of my inbox slot there.
-  constexpr int PUSH_PER = (MAXCS * NCH + NT - 1) / NT;
-  int my_ch[PUSH_PER];
-  uint32_t my_raddr[PUSH_PER], my_rbar[PUSH_PER];
+  // Warp w pushes this CTA's candidate to CTAs w and w + NW (slot rank there).
+  uint32_t push_dst[2][2] = {{0u, 0u}, {0u, 0u}}, push_bar[2][2] = {{0u, 0u}, {0u, 0u}};
+  if (multi)
   {
-    const uint32_t slot0 = smem_addr(&inbox[0][rank]);
-    const uint32_t bar0 = smem_addr(&bars[0]);
 #pragma unroll
-    for (int u = 0; u < PUSH_PER; ++u)
-    {
-      const int idx = t + u * NT;
-      if (idx < CS * NCH)
+    for (int par = 0; par < 2; ++par)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
       {
-        const int dst = idx / NCH, ch = idx % NCH;
-        my_ch[u] = ch;
-        my_raddr[u] = mapa(slot0 + ch * 16, dst);
-        my_rbar[u] = mapa(bar0, dst);
+        const int d = warp + e * NW;
+        if (d < CS)
+        {
+          push_dst[par][e] = mapa(smem_addr(&inbox[par][rank]), d);
+          push_bar[par][e] = mapa(smem_addr(&bars[par]), d);
+        }
       }
-      else
-      {
-        my_ch[u] = -1;
-        my_raddr[u] = my_rbar[u] = 0;
-      }
-    }
   }
 
+#ifdef MPIRG_DEBUG_PANEL
+  long long ptacc[16] = {};
+  long long ptlast = clock64();
+#endif
   T cur[RPT][IB];  // current block columns (registers, static indices)
   int step = 0;    // global step index j (parity / phase bookkeeping)
 #pragma unroll 1
@@ -290,12 +358,11 @@ __global__ void __launch_bounds__(NT, 1)
       {
         if (pos[q] >= k)
         {
-          const double a = fabs(to_d(cur[q][jj]));
-          if (isnan(a))
+          if (is_nan_t(cur[q][jj]))
             nan |= (pos[q] == k);
           else
           {
-            const unsigned long long key = cand_bits(a);
+            const unsigned long long key = mag_key(cur[q][jj]);
             if (key > bkey || (key == bkey && pos[q] < bp))
             {
               bkey = key;
@@ -305,18 +372,18 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
+      PT_MARK(0);
       // 2. warp argmax: max |a|, then min position among ties.
-      const unsigned long long wkey = max_u64_xor(bkey, 32);
-      const int wpos = (int)__reduce_min_sync(0xffffffffu,
-                                              (bkey == wkey && bkey != 0ull) ? (unsigned)bp
-                                                                             : 0x7fffffffu);
+      unsigned long long wkey;
+      int wpos;
+      argmax_redux<WIDE>(bkey, bp, wkey, wpos);
       nan = __any_sync(0xffffffffu, nan);
-      // 3. the warp winner stages header + its block columns + its local row id.
+      // 3. the warp winner stages key, position, block columns, local row id.
       const bool owner = bkey != 0ull && bkey == wkey && bp == wpos;
       if (owner || (lane == 0 && wkey == 0ull))
       {
         WSlot<T> &ws = wslot[par][warp];
-        ws.val = wkey == 0ull ? -1.0 : __longlong_as_double((long long)(wkey - 1ull));
+        ws.key = wkey;
         ws.pos = wkey == 0ull ? INT_MAX : wpos;
         ws.nan = nan;
         ws.lrow = t + bq * NT;
@@ -329,93 +396,128 @@ __global__ void __launch_bounds__(NT, 1)
               ws.blk[c] = cur[q][c];
           }
       }
+      PT_MARK(1);
       __syncthreads();
+      PT_MARK(2);
       // 4. CTA winner over the warp slots (every warp computes it redundantly).
-      const double wv = lane < NW ? wslot[par][lane].val : -1.0;
-      const int wp = lane < NW ? wslot[par][lane].pos : INT_MAX;
-      const unsigned long long ckey0 = (lane < NW && wv >= 0.0) ? cand_bits(wv) : 0ull;
-      const unsigned long long ckey = max_u64_xor(ckey0, 8);
-      const int cp = (int)__reduce_min_sync(0xffffffffu, (ckey0 == ckey && ckey0 != 0ull)
-                                                             ? (unsigned)wp
-                                                             : 0x7fffffffu);
-      const unsigned cmatch = __ballot_sync(0xffffffffu, lane < NW && ckey0 == ckey &&
-                                                             (ckey == 0ull || wp == cp));
-      const int cw = __ffs(cmatch) - 1;
-      const double cv = ckey == 0ull ? -1.0 : __longlong_as_double((long long)(ckey - 1ull));
-      const int cpos = ckey == 0ull ? INT_MAX : cp;
+      const unsigned long long ck0 = lane < NW ? wslot[par][lane].key : 0ull;
+      const int cp0 = lane < NW ? wslot[par][lane].pos : INT_MAX;
+      unsigned long long ckey;
+      int cpos;
+      argmax_redux<WIDE>(ck0, cp0, ckey, cpos);
+      const int cw = __ffs(__ballot_sync(0xffffffffu, lane < NW && ck0 == ckey &&
+                                                          (ckey == 0ull || cp0 == cpos))) -
+                     1;
       const int cn = __any_sync(0xffffffffu, lane < NW ? wslot[par][lane].nan : 0);
-      // 5. push [header | block cols from wslot | right cols from P] to every inbox.
+      if (ckey == 0ull)
+        cpos = INT_MAX;
+      PT_MARK(3);
+      // 5. push the CTA candidate [key|pos|nan|row] to every CTA: warp w sends
+      //    to CTAs w, w+NW, ...; lane l sends 16-byte chunk l (st.async, which
+      //    completes bytes on the receiver's mbarrier). CS == 1: warp 0 just
+      //    assembles it locally.
+      const S *U;
+      int gr = 0;
+      unsigned long long gkey = ckey;
+      int gp = cpos, gn = cn;
+      constexpr int NCH = sizeof(S) / 16;
+      constexpr int EPC = 16 / sizeof(T);
       {
         const WSlot<T> &ws = wslot[par][cw];
         const int lrow = ws.lrow;
-        const int ch_lo = 1 + (int)((jb0 * sizeof(T)) / 16);  // first chunk holding col >= jb0
-        constexpr int EPC = 16 / sizeof(T);                    // elements per chunk
-#pragma unroll
-        for (int u = 0; u < PUSH_PER; ++u)
+        const int ch_lo = 1 + (int)((jb0 * sizeof(T)) / 16);  // chunks left of the block: unused
+        if (multi)
         {
-          const int ch = my_ch[u];
-          if (ch < 0 || (ch != 0 && ch < ch_lo))
-            continue;  // columns left of the block are never read by receivers
-          uint4 val;
-          if (ch == 0)
-          {
-            const unsigned long long vb = (unsigned long long)__double_as_longlong(cv);
-            val = make_uint4((uint32_t)vb, (uint32_t)(vb >> 32), (uint32_t)cpos, (uint32_t)cn);
-          }
-          else
-          {
-            T e[EPC];
 #pragma unroll
-            for (int w = 0; w < EPC; ++w)
+          for (int h = 0; h < (NCH + 31) / 32; ++h)
+          {
+            const int ch = lane + 32 * h;
+            if (ch < NCH && (ch == 0 || ch >= ch_lo))
             {
-              const int c = (ch - 1) * EPC + w;
-              e[w] = (c < bend) ? ws.blk[c - jb0]
-                                : (c < jb && cpos != INT_MAX ? P[c * R + lrow] : T{});
+              uint4 val;
+              if (ch == 0)
+                val = make_uint4((uint32_t)ckey, (uint32_t)(ckey >> 32), (uint32_t)cpos,
+                                 (uint32_t)cn);
+              else
+              {
+                T e[EPC];
+#pragma unroll
+                for (int w = 0; w < EPC; ++w)
+                {
+                  const int c = (ch - 1) * EPC + w;
+                  e[w] = (c < bend) ? ws.blk[c - jb0]
+                                    : ((c < jb && ckey != 0ull) ? P[c * R + lrow] : T{});
+                }
+                val = *reinterpret_cast<const uint4 *>(e);
+              }
+              for (int d = warp; d < CS; d += NW)
+                st_async_v4(push_dst[par][d >= NW] + ch * 16, val, push_bar[par][d >= NW]);
             }
-            val = *reinterpret_cast<const uint4 *>(e);
           }
-          st_async_v4(my_raddr[u] + (uint32_t)(par * MAXCS * sizeof(S)), val,
-                      my_rbar[u] + (uint32_t)(par * sizeof(uint64_t)));
+        }
+        else if (warp == 0)
+        {
+          S &sb = sendbuf[par];
+          if (lane == 0)
+          {
+            sb.key = ckey;
+            sb.pos = cpos;
+            sb.nan = cn;
+          }
+#pragma unroll
+          for (int h = 0; h < (NB + 31) / 32; ++h)
+          {
+            const int c = jb0 + lane + 32 * h;
+            if (c < NB)
+              sb.row[c] = (c < bend) ? ws.blk[c - jb0]
+                                     : ((c < jb && ckey != 0ull) ? P[c * R + lrow] : T{});
+          }
         }
       }
-      // 6. wait until all CS candidates are in my inbox.
-      mbar_wait(&bars[par], (uint32_t)((step >> 1) & 1));
-      // Re-arm this barrier for step+2 now: no peer can send step+2 data before
-      // every CTA (this one included) has pushed step+1, which this thread
-      // precedes in program order.
-      if (t == 0 && step + 2 < jb)
-        mbar_expect_tx(&bars[par], step_bytes(step + 2));
-      // 7. global winner (identical in every thread of every CTA).
-      const double iv = lane < CS ? inbox[par][lane].val : -1.0;
-      const int ip = lane < CS ? inbox[par][lane].pos : INT_MAX;
-      const unsigned long long gkey0 = (lane < CS && iv >= 0.0) ? cand_bits(iv) : 0ull;
-      const unsigned long long gkey = max_u64_xor(gkey0, 16);
-      const int gp = (int)__reduce_min_sync(0xffffffffu, (gkey0 == gkey && gkey0 != 0ull)
-                                                             ? (unsigned)ip
-                                                             : 0x7fffffffu);
-      const unsigned gmatch = __ballot_sync(0xffffffffu, lane < CS && gkey0 == gkey &&
-                                                             (gkey == 0ull || ip == gp));
-      const int gr = __ffs(gmatch) - 1;
-      const int gn = __any_sync(0xffffffffu, lane < CS ? inbox[par][lane].nan : 0);
-      const double gv = gkey == 0ull ? -1.0 : __longlong_as_double((long long)(gkey - 1ull));
+      PT_MARK(4);
+      if (multi)
+      {
+        // 6. wait until all CS candidates are in my inbox, then re-arm the
+        //    barrier for step+2 (no peer can send step+2 data before every CTA,
+        //    this one included, has pushed step+1).
+        mbar_wait(&bars[par], (uint32_t)((step >> 1) & 1));
+        if (t == 0 && step + 2 < jb)
+          mbar_expect_tx(&bars[par], step_bytes(step + 2));
+        PT_MARK(5);
+        // 7. global winner (identical in every thread of every CTA).
+        const unsigned long long gk0 = lane < CS ? inbox[par][lane].key : 0ull;
+        const int gp0 = lane < CS ? inbox[par][lane].pos : INT_MAX;
+        argmax_redux<WIDE>(gk0, gp0, gkey, gp);
+        gr = __ffs(__ballot_sync(0xffffffffu, lane < CS && gk0 == gkey &&
+                                                  (gkey == 0ull || gp0 == gp))) -
+             1;
+        gn = __any_sync(0xffffffffu, lane < CS ? inbox[par][lane].nan : 0);
+        U = &inbox[par][gr];
+      }
+      else
+      {
+        __syncthreads();  // sendbuf assembled by warp 0
+        PT_MARK(5);
+        U = &sendbuf[par];
+      }
       const int p = gn ? k : gp;
-      const T *U = inbox[par][gr].row;
       if (rank == 0 && t == 0)
       {
         ipiv[k] = p;
-        if (!gn && gv == 0.0)
+        if (!gn && gkey == 1ull)  // |pivot| == +0 (key of +0.0)
           atomicMin(&info->singular_col, k);
       }
       // keep the pivot row (stale right columns) for the block-end update
       for (int c = bend + t; c < jb; c += NT)
-        Ub[jj * NB + c] = U[c];
+        Ub[jj * NB + c] = U->row[c];
       if (t < IB)
-        Ub[jj * NB + jb0 + t] = U[jb0 + t];
-      const T piv = U[j];
+        Ub[jj * NB + jb0 + t] = U->row[jb0 + t];
+      const T piv = U->row[j];
       T ub[IB];
 #pragma unroll
       for (int c = jj + 1; c < IB; ++c)
-        ub[c] = U[jb0 + c];
+        ub[c] = U->row[jb0 + c];
+      PT_MARK(6);
       // 8. positions + elimination inside the block (a NaN pivot makes U
       //    irrelevant: l = NaN).
 #pragma unroll
@@ -441,10 +543,12 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       ++step;
+      PT_MARK(7);
     }
 
     // ---- block end: apply the block's rank-1 updates to the columns right
     // of the block, in step order.
+    PT_MARK(9);
     __syncthreads();  // Ub complete
     const int nb_here = bend - jb0;
     // (a) complete the pivot rows: U_jj[c] -= l(pivot jj, jj') * U_jj'[c], jj' < jj
@@ -467,8 +571,10 @@ __global__ void __launch_bounds__(NT, 1)
         Ub[jj * NB + c] = u[jj];
     }
     __syncthreads();
+    PT_MARK(10);
     // (b) every row: its right columns get the updates of the steps at which it
-    //     was still below the pivot (all IB for non-pivot rows).
+    //     was still below the pivot (all IB for non-pivot rows). Four columns
+    //     at a time: independent FMA chains, vector loads of Ub.
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
     {
@@ -479,20 +585,58 @@ __global__ void __launch_bounds__(NT, 1)
       if (pos[q] < 0 || (pos[q] < k0 + jb0 && chosen[q] == IB))
         continue;  // no row, or a pivot of an earlier block
       const int upto = min(chosen[q], nb_here);
-#pragma unroll 4
-      for (int c = bend; c < jb; ++c)
+      T lq[IB];
+#pragma unroll
+      for (int jj = 0; jj < IB; ++jj)
+        lq[jj] = jj < upto ? cur[q][jj] : T{};
+      int c = bend;
+      for (; c + 4 <= jb; c += 4)
+      {
+        T v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          v[e] = P[(c + e) * R + r];
+        T ubv[IB][4];
+#pragma unroll
+        for (int jj = 0; jj < IB; ++jj)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            ubv[jj][e] = Ub[jj * NB + c + e];
+#pragma unroll
+        for (int jj = 0; jj < IB; ++jj)
+          if (jj < upto)
+          {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              v[e] = upd(v[e], lq[jj], ubv[jj][e]);
+          }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          P[(c + e) * R + r] = v[e];
+      }
+      for (; c < jb; ++c)
       {
         T v = P[c * R + r];
 #pragma unroll
         for (int jj = 0; jj < IB; ++jj)
           if (jj < upto)
-            v = upd(v, cur[q][jj], Ub[jj * NB + c]);
+            v = upd(v, lq[jj], Ub[jj * NB + c]);
         P[c * R + r] = v;
       }
     }
     __syncthreads();
+    PT_MARK(11);
   }
 
+  PT_MARK(8);
+#ifdef MPIRG_DEBUG_PANEL
+  if (t == 0 && rank == 0 && (k0 == 0 || k0 + jb >= n))
+    printf("panel k0=%d CS=%d steps=%d cycles/step: cand %lld warp %lld sync %lld cta %lld push %lld "
+           "wait %lld glob %lld upd %lld | per panel: (a) %lld (b) %lld | push: wg %lld gather %lld fence %lld\n",
+           k0, CS, step, ptacc[0] / step, ptacc[1] / step, ptacc[2] / step, ptacc[3] / step,
+           ptacc[4] / step, ptacc[5] / step, ptacc[6] / step, ptacc[7] / step, ptacc[10],
+           ptacc[11], ptacc[12] / step, ptacc[13] / step, ptacc[14] / step);
+#endif
   // Write every row to its final position; record the row moves.
 #pragma unroll
   for (int q = 0; q < RPT; ++q)
@@ -509,7 +653,10 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
   }
-  cluster_sync_all();  // no CTA may exit while peers can still write its inbox
+  if (multi)
+  {
+    cluster_sync_all();  // no CTA may exit while peers can still write its inbox
+  }
 }
 
 }  // namespace panel2
