@@ -71,6 +71,13 @@ def update_parms(cr=None, ce=None, rmax=None, litmax=None) -> L.mpirg_term_param
     nan = float("nan")
     if litmax is not None and litmax < 1:
         raise InvalidParameter("litmax must be at least 1")
+    # NaN means "not given" at the C-ABI; an explicit NaN must fail validation
+    # like the reference's TermParams::validate (ir_engine.hpp:40-45).
+    for nm, v in (("cr", cr), ("ce", ce)):
+        if v is not None and not (v == v):
+            raise InvalidParameter(f"{nm} must be positive and finite")
+    if rmax is not None and not (rmax == rmax):
+        raise InvalidParameter("rmax must lie in (0, 1]")
     st = L.lib().mpirg_update_parms(nan if cr is None else float(cr),
                                     nan if ce is None else float(ce),
                                     nan if rmax is None else float(rmax),
