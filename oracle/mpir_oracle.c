@@ -800,7 +800,9 @@ int orc_ir(int tw, int tf, int tr, int on_the_fly, int resid_term, int n, const 
     {
       const int small = resid_term
                             ? rnew <= cr * eps_w * bnorm
-                            : rnew <= ce * eps_w * (bnorm + *a_norm1 * orc_norm_inf(tr, x, n));
+                            /* GCC contracts bnorm + a_norm1*||x|| under the reference's
+                               flags (verified on the -O3 -march build): one fma */
+                            : rnew <= ce * eps_w * fma(*a_norm1, orc_norm_inf(tr, x, n), bnorm);
       if (small)
       {
         *reason = resid_term ? R_SMALL_RESIDUAL : R_SMALL_BACKWARD;

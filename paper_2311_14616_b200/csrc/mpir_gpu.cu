@@ -14,12 +14,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <climits>
 #include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/mpir_gpu.h"
@@ -390,8 +392,10 @@ struct mpirg_factorization
       }
       if (!extended)
       {
+        // ir_engine.hpp:234-236; the reference build contracts
+        // bnorm + a_norm1 * ||x|| into one fma (GCC, -O3 -march, FMA host).
         const bool small = cfg.resid_term ? rnew <= tp.cr * eps_w * bnorm
-                                          : rnew <= tp.ce * eps_w * (bnorm + anorm1 * xnorm);
+                                          : rnew <= tp.ce * eps_w * std::fma(anorm1, xnorm, bnorm);
         if (small)
         {
           reason = cfg.resid_term ? MPIRG_SMALL_RESIDUAL : MPIRG_SMALL_BACKWARD_ERROR;
@@ -578,7 +582,7 @@ int mpirg_factorization_create(mpirg_factorization **out, int n, const mpirg_con
     try
     {
       f->alloc();
-      if (n > 0)
+      if (n > 0 && a)  // a == NULL: allocate only (refactor supplies A later)
       {
         MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->a_high, a, (size_t)n * n * f->tw_bytes(),
                                          a_on_device ? cudaMemcpyDeviceToDevice
@@ -912,64 +916,128 @@ int mpirg_residual(int tw, int tr, int n, const void *a, const void *x, const vo
   });
 }
 
+// Config 5b: independent systems solved concurrently. W host workers, each
+// driving its own handle (own streams, workspaces and pinned mirrors), take
+// systems from a shared counter; their kernels overlap on the SMs that one
+// N~1024 system leaves idle. Each system is exactly one MPFactorization +
+// ir_solve_report, so results equal the sequential ones bit for bit.
+static int batch_workers(int count, int n)
+{
+  int w = n <= 1024 ? 16 : (n <= 2048 ? 8 : (n <= 4096 ? 4 : 1));
+  if (const char *e = std::getenv("MPIRG_BATCH_WORKERS"))
+    w = std::max(1, std::atoi(e));
+  return std::max(1, std::min(w, count));
+}
+
 int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *a, const void *b,
                          int on_device, const mpirg_term_params *tp, void *sol, double *rhist,
                          double *dhist, int hist_capacity, int *rhist_len, int *reason,
                          int *status, double *device_ms, mpirg_error *err)
 {
-  int first = MPIRG_OK;
-  mpirg_error local{};
-  mpirg_factorization *f = nullptr;
-  mpirg_config c = *cfg;
-  const size_t tw = elem_size(c.tw);
-  double ms = 0.0;
-  for (int sidx = 0; sidx < count; ++sidx)
+  if (count <= 0)
   {
-    const char *as = static_cast<const char *>(a) + (size_t)sidx * n * n * tw;
-    const char *bs = static_cast<const char *>(b) + (size_t)sidx * n * tw;
-    int st;
-    if (!f)
-    {
-      st = mpirg_factorization_create(&f, n, &c, as, on_device, &local);
-      if (!f)
-      {
-        status[sidx] = st;
-        if (first == MPIRG_OK)
-        {
-          first = st;
-          if (err)
-            *err = local;
-        }
-        continue;
-      }
-    }
-    else
-      st = mpirg_factorization_refactor(f, as, on_device, &local);
-    if (st == MPIRG_OK)
-    {
-      ms += f->factor_ms;
-      mpirg_report rep{};
-      rep.sol = static_cast<char *>(sol) + (size_t)sidx * n * tw;
-      rep.sol_on_device = on_device;
-      rep.rhist = rhist + (size_t)sidx * hist_capacity;
-      rep.dhist = dhist + (size_t)sidx * hist_capacity;
-      rep.hist_capacity = hist_capacity;
-      st = mpirg_ir_solve(f, bs, on_device, tp, &rep, &local);
-      rhist_len[sidx] = rep.rhist_len;
-      reason[sidx] = rep.reason;
-      ms += rep.solve_ms;
-    }
-    status[sidx] = st;
-    if (st != MPIRG_OK && first == MPIRG_OK)
+    if (device_ms)
+      *device_ms = 0.0;
+    fill_err(err, MPIRG_OK, "");
+    return MPIRG_OK;
+  }
+  int dev = 0;
+  if (cfg->device >= 0)
+    cudaSetDevice(cfg->device);
+  cudaGetDevice(&dev);
+  const int W = batch_workers(count, n);
+  const size_t tw = elem_size(cfg->tw);
+  std::atomic<int> next{0};
+  std::mutex emu;
+  int first = MPIRG_OK;
+  mpirg_error first_err{};
+  auto note = [&](int st, const mpirg_error &e) {
+    std::lock_guard<std::mutex> lk(emu);
+    if (first == MPIRG_OK && st != MPIRG_OK)
     {
       first = st;
+      first_err = e;
+    }
+  };
+  cudaEvent_t start = nullptr;
+  std::vector<cudaEvent_t> ends(W, nullptr);
+  std::vector<int> used(W, 0);
+  {
+    mpirg_error e{};
+    const int st = guarded(&e, [&] {
+      MPIRG_CUDA_CHECK(cudaEventCreate(&start));
+      for (auto &ev : ends)
+        MPIRG_CUDA_CHECK(cudaEventCreate(&ev));
+      MPIRG_CUDA_CHECK(cudaEventRecord(start, 0));
+    });
+    if (st != MPIRG_OK)
+    {
       if (err)
-        *err = local;
+        *err = e;
+      return st;
     }
   }
-  mpirg_factorization_destroy(f);
+  auto worker = [&](int w) {
+    cudaSetDevice(dev);
+    mpirg_config c = *cfg;
+    c.device = dev;
+    mpirg_error e{};
+    mpirg_factorization *f = nullptr;
+    int st = mpirg_factorization_create(&f, n, &c, nullptr, on_device, &e);
+    if (st != MPIRG_OK)
+    {
+      note(st, e);
+      for (int sidx; (sidx = next.fetch_add(1)) < count;)
+        status[sidx] = st;
+      return;
+    }
+    cudaStreamWaitEvent(f->stream, start, 0);
+    for (int sidx; (sidx = next.fetch_add(1)) < count;)
+    {
+      const char *as = static_cast<const char *>(a) + (size_t)sidx * n * n * tw;
+      const char *bs = static_cast<const char *>(b) + (size_t)sidx * n * tw;
+      rhist_len[sidx] = 0;
+      reason[sidx] = MPIRG_ITERATION_LIMIT;
+      st = mpirg_factorization_refactor(f, as, on_device, &e);
+      if (st == MPIRG_OK)
+      {
+        mpirg_report rep{};
+        rep.sol = static_cast<char *>(sol) + (size_t)sidx * n * tw;
+        rep.sol_on_device = on_device;
+        rep.rhist = rhist + (size_t)sidx * hist_capacity;
+        rep.dhist = dhist + (size_t)sidx * hist_capacity;
+        rep.hist_capacity = hist_capacity;
+        st = mpirg_ir_solve(f, bs, on_device, tp, &rep, &e);
+        rhist_len[sidx] = rep.rhist_len;
+        reason[sidx] = rep.reason;
+      }
+      status[sidx] = st;
+      note(st, e);
+    }
+    cudaEventRecord(ends[w], f->stream);
+    cudaEventSynchronize(ends[w]);
+    used[w] = 1;
+    mpirg_factorization_destroy(f);
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < W; ++w)
+    pool.emplace_back(worker, w);
+  worker(0);
+  for (auto &t : pool)
+    t.join();
+  double ms = 0.0;
+  for (int w = 0; w < W; ++w)
+  {
+    float m = 0.0f;
+    if (used[w] && cudaEventElapsedTime(&m, start, ends[w]) == cudaSuccess)
+      ms = std::max(ms, (double)m);
+    cudaEventDestroy(ends[w]);
+  }
+  cudaEventDestroy(start);
   if (device_ms)
     *device_ms = ms;
+  if (err)
+    *err = first == MPIRG_OK ? mpirg_error{} : first_err;
   if (first == MPIRG_OK)
     fill_err(err, MPIRG_OK, "");
   return first;

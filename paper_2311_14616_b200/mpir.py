@@ -266,6 +266,60 @@ def solve(a, b, *, working="double", factor=None, residual=None, on_the_fly=None
     return f._solve_device(_to_device_working(b, f._cfg.tw), tp)
 
 
+def batch_solve(a, b, *, working="double", factor=None, residual=None, on_the_fly=None,
+                resid_term=True, cr=None, ce=None, rmax=None, litmax=None, device=None,
+                raise_on_error=True) -> list[dict]:
+    """Config 5b: ``count`` independent systems, each exactly one
+    MPFactorization + ir_solve_report (concurrent solves use
+    separate objects). ``a``: (count, n, n) float64 (row-major matrices) or a
+    CUDA tensor of TW holding count column-major n*n blocks; ``b``: (count, n).
+    The systems run concurrently on the device (mpirg_batch_ir_solve)."""
+    torch = _torch()
+    tp = update_parms(cr, ce, rmax, litmax)
+    cfg = resolve_config(parse_precision(working),
+                         None if factor is None else parse_precision(factor),
+                         None if residual is None else parse_precision(residual), on_the_fly)
+    cfg.resid_term = int(bool(resid_term))
+    cfg.device = -1 if device is None else int(device)
+    if isinstance(a, torch.Tensor):
+        adev, bdev = a, b
+        count = b.shape[0]
+        n = b.shape[1]
+    else:
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 3 or a.shape[1] != a.shape[2]:
+            raise DimensionMismatch("batch matrices must be (count, n, n)")
+        count, n = a.shape[0], a.shape[1]
+        adev = _to_device_working(np.ascontiguousarray(np.transpose(a, (0, 2, 1))), cfg.tw)
+        bdev = _to_device_working(np.asarray(b, dtype=np.float64).reshape(count, n), cfg.tw)
+    sol = torch.empty((count, n), dtype=bdev.dtype, device=bdev.device)
+    cap = tp.litmax + 1
+    rh = np.zeros((count, cap))
+    dh = np.zeros((count, cap))
+    rlen = np.zeros(count, dtype=np.int32)
+    reason = np.zeros(count, dtype=np.int32)
+    status = np.zeros(count, dtype=np.int32)
+    ms = C.c_double(0.0)
+    err = L.mpirg_error()
+    torch.cuda.current_stream().synchronize()
+    st = L.lib().mpirg_batch_ir_solve(count, n, C.byref(cfg), adev.data_ptr(), bdev.data_ptr(),
+                                      1, C.byref(tp), sol.data_ptr(), rh.ctypes.data,
+                                      dh.ctypes.data, cap, rlen.ctypes.data,
+                                      reason.ctypes.data, status.ctypes.data, C.byref(ms),
+                                      C.byref(err))
+    if st != 0 and raise_on_error:
+        L.check(st, err)
+    x = sol.double().cpu().numpy()
+    out = []
+    for i in range(count):
+        k = int(rlen[i])
+        out.append({"x": x[i], "rhist": list(rh[i, :k]), "dhist": list(dh[i, :max(k - 1, 0)]),
+                    "khist": [], "status": int(status[i]),
+                    "reason": L.REASONS[int(reason[i])] if status[i] == 0 else None})
+    batch_solve.last_device_ms = ms.value
+    return out
+
+
 # ---- problem generators (greens.cpp; inputs, not the timed path) ----------
 def build_operator(n: int, alpha: float) -> np.ndarray:
     """I - alpha*G (greens.cpp:48-59), bitwise the reference's."""
@@ -310,5 +364,5 @@ def greens_problem(n: int, alpha: float, rhs: str = "manufactured") -> dict:
 
 __all__ = ["DimensionMismatch", "Factorization", "InvalidConfig", "InvalidParameter",
            "NonFiniteResult", "NotConverged", "OverflowDetected", "SingularPivot",
-           "__version__", "build_operator", "greens_matrix", "greens_problem",
+           "__version__", "batch_solve", "build_operator", "greens_matrix", "greens_problem",
            "machine_eps", "solve", "unit_roundoff", "resolve_config", "update_parms"]
