@@ -141,7 +141,8 @@ double mpirg_unit_roundoff(int precision); /* precision.hpp:28-39 */
  * ------------------------------------------------------------------------- */
 /* Constructor: takes a copy of the TW matrix a (host or device memory), then
  * refactor(): one-norm of a_high in TW, demotion into the factor storage with
- * overflow/underflow checks, LU in place. */
+ * overflow/underflow checks, LU in place. a == NULL allocates only (no
+ * factorization yet: call refactor or cast + set_factored before solving). */
 int mpirg_factorization_create(mpirg_factorization **out, int n, const mpirg_config *cfg,
                                const void *a, int a_on_device, mpirg_error *err);
 /* refactor(const Matrix<TW>&) (mp_structures.hpp:155-169). a == NULL
@@ -219,6 +220,57 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
                          void *sol, double *rhist, double *dhist, int hist_capacity,
                          int *rhist_len, int *reason, int *status, double *device_ms,
                          mpirg_error *err);
+
+/* ---------------------------------------------------------------------------
+ * Config 5a: the 1-D block-cyclic LU across ranks.
+ * One handle per rank (one process per GPU). Column block b (block_cols
+ * columns, a power of two and a multiple of nb; <= 0 picks 256) lives on
+ * rank b mod nranks. Each rank holds an n x n factor buffer `a` (TF,
+ * column-major, ld n; B200's 180 GB holds the full fp32 matrix of N=65536
+ * per GPU) of which it owns its column blocks. Per panel p:
+ *   owner:   mpirg_dlu_panel -> mpirg_dlu_pack(msg)
+ *   all:     broadcast msg (mpirg_dlu_msg_bytes(p) bytes) from the owner
+ *   others:  mpirg_dlu_unpack(msg)
+ *   all:     mpirg_dlu_update(part 1 = next panel's columns if owned, then
+ *            part 2 = the rest on the handle's side stream; or part 0 = all)
+ * The factors, pivots and moves are bit-identical to the single-GPU LU
+ * (detail::lu_inplace, dense_lu.hpp:63-107) for every nranks. Reference: no
+ * counterpart (the reference is single-process); the per-element order is
+ * the blocked equivalence of SURVEY.md 8(c).
+ * ------------------------------------------------------------------------- */
+typedef struct mpirg_dlu mpirg_dlu;
+int mpirg_dlu_create(mpirg_dlu **out, int prec, int n, int nb, int nranks, int rank,
+                     int block_cols, int device, mpirg_error *err);
+void mpirg_dlu_destroy(mpirg_dlu *h);
+int mpirg_dlu_nb(const mpirg_dlu *h);
+int mpirg_dlu_npanels(const mpirg_dlu *h);
+int mpirg_dlu_block_cols(const mpirg_dlu *h);
+int mpirg_dlu_owner(const mpirg_dlu *h, int p);
+size_t mpirg_dlu_msg_bytes(const mpirg_dlu *h, int p);
+/* perm (optional, device int[n]) receives the row permutation (rank 0). */
+int mpirg_dlu_begin(mpirg_dlu *h, int *perm, void *stream, mpirg_error *err);
+int mpirg_dlu_panel(mpirg_dlu *h, void *a, int p, int *ipiv, void *stream, mpirg_error *err);
+int mpirg_dlu_pack(mpirg_dlu *h, const void *a, int p, const int *ipiv, void *msg,
+                   void *stream, mpirg_error *err);
+int mpirg_dlu_unpack(mpirg_dlu *h, void *a, int p, int *ipiv, const void *msg, void *stream,
+                     mpirg_error *err);
+int mpirg_dlu_update(mpirg_dlu *h, void *a, int p, int part, int *perm, void *stream,
+                     mpirg_error *err);
+/* Joins the side stream into `stream`, synchronises, and returns the first
+ * exactly-zero pivot column seen by this rank (-1 = none). */
+int mpirg_dlu_end(mpirg_dlu *h, void *stream, int *singular_col, mpirg_error *err);
+
+/* A handle whose LU is computed elsewhere (the distributed LU on rank 0):
+ * _cast runs MPFactorization::refactor up to and including the demotion
+ * (A_F in the handle's factor buffer, ||A||_1, overflow/underflow checks);
+ * _buffers exposes the device factor buffer, ipiv, perm and stream;
+ * _set_factored validates the external factorization (SingularPivot). */
+int mpirg_factorization_cast(mpirg_factorization *f, const void *a, int a_on_device,
+                             mpirg_error *err);
+int mpirg_factorization_buffers(mpirg_factorization *f, void **a_low, int **ipiv, int **perm,
+                                void **stream);
+int mpirg_factorization_set_factored(mpirg_factorization *f, int singular_col,
+                                     mpirg_error *err);
 
 /* ---------------------------------------------------------------------------
  * Measurement hooks (bench.py): per-kernel-class CUDA-event timing and an

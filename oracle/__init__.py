@@ -76,6 +76,8 @@ class CpuImpl:
             f("f2h", C.c_uint16, [C.c_float])
             f("d2h", C.c_uint16, [C.c_double])
             f("h2f", C.c_float, [C.c_uint16])
+            f("dlu_panel", _I, [_I, _I, _P, _I, _I, _IP, _IP, _IP, _IP])
+            f("dlu_update", _I, [_I, _I, _P, _I, _I, _IP, _I, _I, _I, _I, _I, _I, _I, _IP])
         else:
             f("ir", _I, [_I, _I, _I, _I, _I, _I, _P, _P, _D, _D, _D, _I, _P, _DP, _DP, _IP,
                          _IP, _IP, _P, _DP, _IP, _IP, _DP, _DP, _DP])
@@ -118,6 +120,26 @@ class CpuImpl:
         st = self._lu(prec, n, _ptr(a), ipiv.ctypes.data_as(_IP), perm.ctypes.data_as(_IP),
                       C.byref(sc))
         return st, a, ipiv, perm, sc.value
+
+    # -- blocked steps of the distributed LU (restatement only) ---------------
+    def dlu_panel(self, prec, a_ptr, n, k0, jb, ipiv: np.ndarray, singular: list):
+        """Panel step on a rank's n*n buffer at a_ptr; returns the (dst, src) moves."""
+        moves = np.zeros(2 * 2 * jb, dtype=np.int32)
+        nm = C.c_int(0)
+        sc = C.c_int(singular[0])
+        st = self._dlu_panel(prec, n, C.c_void_p(a_ptr), k0, jb, ipiv.ctypes.data_as(_IP),
+                             moves.ctypes.data_as(_IP), C.byref(nm), C.byref(sc))
+        assert st == 0
+        singular[0] = sc.value
+        return moves[: 2 * nm.value].reshape(-1, 2).copy()
+
+    def dlu_update(self, prec, a_ptr, n, k0, jb, moves: np.ndarray, G, r, sh, cb, ce, left,
+                   perm: np.ndarray | None):
+        mv = np.ascontiguousarray(moves, dtype=np.int32).reshape(-1)
+        st = self._dlu_update(prec, n, C.c_void_p(a_ptr), k0, jb, mv.ctypes.data_as(_IP),
+                              mv.size // 2, G, r, sh, cb, ce, left,
+                              None if perm is None else perm.ctypes.data_as(_IP))
+        assert st == 0
 
     def solve_mps(self, ts, tf, packed, ipiv, x):
         x = np.array(x, dtype=DTYPES[ts], copy=True)

@@ -339,6 +339,158 @@ int orc_lu(int p, int n, void *a, int *ipiv, int *perm, int *singular_col)
   return lu_f16((uint16_t *)a, n, ipiv, perm, singular_col);
 }
 
+/* ------------------------------------------------------------------------ */
+/* Blocked building blocks of the 1-D block-cyclic LU (config 5a), used only */
+/* by the multi-process CPU tests of the distributed schedule. Restated from */
+/* lu_inplace (dense_lu.hpp:63-107) in its blocked right-looking form, whose */
+/* per-element FMA order equals the unblocked loop.         */
+/*   panel: the column loop restricted to columns [k0, k0+jb); the row swaps */
+/*          touch only those columns; the composed swaps are returned as a   */
+/*          gather list new[dst] = old[src] (<= 2 jb entries).               */
+/*   update: that gather on owned columns outside the panel, then for owned  */
+/*          trailing columns U12 = L11^-1 A12 (k ascending) and              */
+/*          A22 = fma(-L21, U12, A22) (k ascending).                         */
+/* A zero pivot column is recorded (first one) and the step continues with   */
+/* p = k, as the device panel does.                                          */
+/* ------------------------------------------------------------------------ */
+#define DEFINE_DLU(SUF, T, ABSD, DIV, UPD)                                         \
+  static void dlu_panel_##SUF(T *a, int n, int k0, int jb, int *ipiv, int *moves,  \
+                              int *nmoves, int *singular)                          \
+  {                                                                                \
+    const int m = n - k0;                                                          \
+    int *pp = (int *)malloc(sizeof(int) * (size_t)(m > 0 ? m : 1));               \
+    for (int i = 0; i < m; ++i)                                                    \
+      pp[i] = k0 + i;                                                              \
+    for (int k = k0; k < k0 + jb; ++k)                                             \
+    {                                                                              \
+      T *ck = a + (int64_t)k * n;                                                  \
+      int p = k;                                                                   \
+      double best = ABSD(ck[k]);                                                   \
+      for (int i = k + 1; i < n; ++i)                                              \
+      {                                                                            \
+        const double v = ABSD(ck[i]);                                              \
+        if (v > best)                                                              \
+        {                                                                          \
+          best = v;                                                                \
+          p = i;                                                                   \
+        }                                                                          \
+      }                                                                            \
+      if (best == 0.0 && *singular < 0)                                            \
+        *singular = k;                                                             \
+      ipiv[k] = p;                                                                 \
+      if (p != k)                                                                  \
+      {                                                                            \
+        for (int64_t j = k0; j < k0 + jb; ++j)                                     \
+        {                                                                          \
+          T t = a[j * n + k];                                                      \
+          a[j * n + k] = a[j * n + p];                                             \
+          a[j * n + p] = t;                                                        \
+        }                                                                          \
+        int t = pp[k - k0];                                                        \
+        pp[k - k0] = pp[p - k0];                                                   \
+        pp[p - k0] = t;                                                            \
+      }                                                                            \
+      const T piv = ck[k];                                                         \
+      for (int i = k + 1; i < n; ++i)                                              \
+        ck[i] = DIV(ck[i], piv);                                                   \
+      for (int64_t j = k + 1; j < k0 + jb; ++j)                                    \
+      {                                                                            \
+        T *cj = a + j * n;                                                         \
+        const T ukj = cj[k];                                                       \
+        for (int i = k + 1; i < n; ++i)                                            \
+          cj[i] = UPD(cj[i], ck[i], ukj);                                          \
+      }                                                                            \
+    }                                                                              \
+    int e = 0;                                                                     \
+    for (int i = 0; i < m; ++i)                                                    \
+      if (pp[i] != k0 + i)                                                         \
+      {                                                                            \
+        moves[2 * e] = k0 + i;                                                     \
+        moves[2 * e + 1] = pp[i];                                                  \
+        ++e;                                                                       \
+      }                                                                            \
+    *nmoves = e;                                                                   \
+    free(pp);                                                                      \
+  }                                                                                \
+  static void gather_##SUF(T *col, const int *moves, int nm, T *tmp)               \
+  {                                                                                \
+    for (int e = 0; e < nm; ++e)                                                   \
+      tmp[e] = col[moves[2 * e + 1]];                                              \
+    for (int e = 0; e < nm; ++e)                                                   \
+      col[moves[2 * e]] = tmp[e];                                                  \
+  }                                                                                \
+  static void dlu_update_##SUF(T *a, int n, int k0, int jb, const int *moves,      \
+                               int nm, int G, int r, int sh, int cb, int ce,       \
+                               int left)                                           \
+  {                                                                                \
+    T tmp[256];                                                                    \
+    for (int64_t c = 0; c < n; ++c)                                                \
+    {                                                                              \
+      if (G > 1 && ((int)(c >> sh) % G) != r)                                      \
+        continue;                                                                  \
+      T *cc = a + c * n;                                                           \
+      if (left && c < k0)                                                          \
+        gather_##SUF(cc, moves, nm, tmp);                                          \
+      if (c < cb || c >= ce)                                                       \
+        continue;                                                                  \
+      gather_##SUF(cc, moves, nm, tmp);                                            \
+      for (int kk = 0; kk < jb; ++kk)                                              \
+      {                                                                            \
+        const T *lk = a + (int64_t)(k0 + kk) * n;                                  \
+        const T x = cc[k0 + kk];                                                   \
+        for (int i = k0 + kk + 1; i < k0 + jb; ++i)                                \
+          cc[i] = UPD(cc[i], lk[i], x);                                            \
+      }                                                                            \
+      for (int kk = 0; kk < jb; ++kk)                                              \
+      {                                                                            \
+        const T *lk = a + (int64_t)(k0 + kk) * n;                                  \
+        const T u = cc[k0 + kk];                                                   \
+        for (int i = k0 + jb; i < n; ++i)                                          \
+          cc[i] = UPD(cc[i], lk[i], u);                                            \
+      }                                                                            \
+    }                                                                              \
+  }
+
+DEFINE_DLU(f64, double, ABS_D64, DIV_NATIVE, UPD_F64)
+DEFINE_DLU(f32, float, ABS_D32, DIV_NATIVE, UPD_F32)
+
+int orc_dlu_panel(int p, int n, void *a, int k0, int jb, int *ipiv, int *moves, int *nmoves,
+                  int *singular)
+{
+  if (p == B64)
+    dlu_panel_f64((double *)a, n, k0, jb, ipiv, moves, nmoves, singular);
+  else if (p == B32)
+    dlu_panel_f32((float *)a, n, k0, jb, ipiv, moves, nmoves, singular);
+  else
+    return ST_CONFIG;
+  return ST_OK;
+}
+
+/* Owned columns (block 2^sh, block b on rank b mod G) in [cb, ce) get the
+ * step's gather + U12 + A22 update; left != 0 also gathers owned columns
+ * < k0; perm (optional) is gathered too. */
+int orc_dlu_update(int p, int n, void *a, int k0, int jb, const int *moves, int nmoves, int G,
+                   int r, int sh, int cb, int ce, int left, int *perm)
+{
+  if (nmoves > 256)
+    return ST_CONFIG;
+  if (perm && left)
+  {
+    int tmp[256];
+    for (int e = 0; e < nmoves; ++e)
+      tmp[e] = perm[moves[2 * e + 1]];
+    for (int e = 0; e < nmoves; ++e)
+      perm[moves[2 * e]] = tmp[e];
+  }
+  if (p == B64)
+    dlu_update_f64((double *)a, n, k0, jb, moves, nmoves, G, r, sh, cb, ce, left);
+  else if (p == B32)
+    dlu_update_f32((float *)a, n, k0, jb, moves, nmoves, G, r, sh, cb, ce, left);
+  else
+    return ST_CONFIG;
+  return ST_OK;
+}
+
 /* detail::apply_pivots (dense_lu.hpp:37-44) */
 #define DEFINE_PIV(NAME, T)                                                        \
   static void NAME(const int *ipiv, int n, T *x)                                   \

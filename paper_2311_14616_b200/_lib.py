@@ -132,6 +132,23 @@ PROTOTYPES = {
     "mpirg_solve_mps": (_I, [_I, _I, _I, _P, _P, _P, _P, _E]),
     "mpirg_solve_lps": (_I, [_I, _I, _I, _P, _P, _P, _P, C.POINTER(C.c_int), _P, _E]),
     "mpirg_residual": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _E]),
+    "mpirg_factorization_cast": (_I, [_H, _P, _I, _E]),
+    "mpirg_factorization_buffers": (_I, [_H, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                         C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "mpirg_factorization_set_factored": (_I, [_H, _I, _E]),
+    "mpirg_dlu_create": (_I, [C.POINTER(_H), _I, _I, _I, _I, _I, _I, _I, _E]),
+    "mpirg_dlu_destroy": (None, [_H]),
+    "mpirg_dlu_nb": (_I, [_H]),
+    "mpirg_dlu_npanels": (_I, [_H]),
+    "mpirg_dlu_block_cols": (_I, [_H]),
+    "mpirg_dlu_owner": (_I, [_H, _I]),
+    "mpirg_dlu_msg_bytes": (_S, [_H, _I]),
+    "mpirg_dlu_begin": (_I, [_H, _P, _P, _E]),
+    "mpirg_dlu_panel": (_I, [_H, _P, _I, _P, _P, _E]),
+    "mpirg_dlu_pack": (_I, [_H, _P, _I, _P, _P, _P, _E]),
+    "mpirg_dlu_unpack": (_I, [_H, _P, _I, _P, _P, _P, _E]),
+    "mpirg_dlu_update": (_I, [_H, _P, _I, _I, _P, _P, _E]),
+    "mpirg_dlu_end": (_I, [_H, _P, C.POINTER(C.c_int), _E]),
     "mpirg_batch_ir_solve": (_I, [_I, _I, C.POINTER(mpirg_config), _P, _P, _I,
                                   C.POINTER(mpirg_term_params), _P, _P, _P, _I, _P, _P, _P,
                                   C.POINTER(C.c_double), _E]),

@@ -68,6 +68,9 @@ struct LuWorkspace
   int *nmoves = nullptr;  // [npanels]
   void *side = nullptr;   // cudaStream_t: look-ahead side stream
   void *events = nullptr; // cudaEvent_t[3*npanels]
+  int *pp = nullptr;      // [n] composed row map of a tall panel
+  int2 *smv = nullptr;    // [2*nb] row moves of the tall panel's 8-column leaves
+  int *snm = nullptr;     // [nb/8]
 };
 // Chooses the panel width for n and the factor precision (0 = auto).
 int lu_choose_nb(int prec, int n, int requested);
@@ -81,6 +84,25 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
                DevInfo *info, cudaStream_t s);
 // perm from ipiv for callers that only hold ipiv (standalone solves).
 void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s);
+
+// One rank of the 1-D block-cyclic LU (config 5a). a is the
+// rank's n x n factor buffer (ld n) of which it owns the column blocks
+// b with b mod G == r (block_cols columns each, a power-of-two multiple of
+// nb); the broadcast of each panel between ranks is the caller's.
+struct DluPlan
+{
+  int prec = 0, n = 0, G = 1, r = 0, sh = 30;
+  LuWorkspace ws;
+};
+void dlu_alloc(DluPlan &d, int prec, int n, int nb, int G, int r, int block_cols);
+void dlu_free(DluPlan &d);
+void dlu_begin(DluPlan &d, int *perm, cudaStream_t s);
+void dlu_panel(DluPlan &d, void *a, int p, int *ipiv, DevInfo *info, cudaStream_t s);
+// part 0: whole step on s; 1: the next panel's columns (if owned) on s;
+// 2: the remaining owned columns + left-column moves on the side stream.
+void dlu_update(DluPlan &d, void *a, int p, int part, int *perm, cudaStream_t s);
+void dlu_end(DluPlan &d, cudaStream_t s);
+void dlu_merge_singular(int *dst, const int *src, cudaStream_t s);
 
 // ---- K6: triangular solves ------------------------------------------------
 struct TrsvWorkspace

@@ -49,11 +49,37 @@ namespace mpirg
 namespace
 {
 
+// Column ownership of a rank under the 1-D block-cyclic distribution of
+// BASELINE config 5a: global column blocks of 2^sh columns,
+// block b on rank b mod G. Kernels walk the rank's columns by LOCAL index L
+// (owned columns in ascending global order) and map L to the global column.
+// G == 1 is the identity (single-GPU LU).
+struct ColMap
+{
+  int G = 1, r = 0, sh = 30;
+  __host__ __device__ __forceinline__ int g(int L) const
+  {
+    if (G == 1)
+      return L;
+    const int m = (1 << sh) - 1;
+    return ((((L >> sh) * G) + r) << sh) | (L & m);
+  }
+  // number of owned columns with global index < c
+  __host__ __device__ int lcount(int c) const
+  {
+    if (G == 1)
+      return c;
+    const int full = c >> sh;
+    const int owned = full > r ? (full - 1 - r) / G + 1 : 0;
+    return (owned << sh) + ((full % G) == r ? (c & ((1 << sh) - 1)) : 0);
+  }
+};
+
 // Gather-apply the panel's row moves (new[dst] = old[src]) to the columns
 // [cb, ce) -- one warp per column -- and to perm (block 0, warp 0).
 template <typename T, int NB>
 __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, int n, int cb,
-                                                             int ce,
+                                                             int ce, ColMap map,
                                                              const int2 *__restrict__ moves,
                                                              const int *__restrict__ nmoves,
                                                              int *__restrict__ perm)
@@ -94,7 +120,7 @@ __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, 
     for (int u = 0; u < UNR; ++u)
       if (c0 + u < ncols)
       {
-        const T *cp = A + (size_t)(cb + c0 + u) * n;
+        const T *cp = A + (size_t)map.g(cb + c0 + u) * n;
 #pragma unroll
         for (int q = 0; q < PER; ++q)
           if (mv[q].x >= 0)
@@ -105,7 +131,7 @@ __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, 
     for (int u = 0; u < UNR; ++u)
       if (c0 + u < ncols)
       {
-        T *cp = A + (size_t)(cb + c0 + u) * n;
+        T *cp = A + (size_t)map.g(cb + c0 + u) * n;
 #pragma unroll
         for (int q = 0; q < PER; ++q)
           if (mv[q].x >= 0)
@@ -124,7 +150,7 @@ __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, 
 constexpr int MT_COLS = 32;
 template <typename T, int NB>
 __global__ void __launch_bounds__(128) lu_mt_kernel(T *__restrict__ A, int n, int k0, int jb,
-                                                    int cb, int ce,
+                                                    int cb, int ce, ColMap map,
                                                     const int2 *__restrict__ moves,
                                                     const int *__restrict__ nmoves)
 {
@@ -169,7 +195,7 @@ __global__ void __launch_bounds__(128) lu_mt_kernel(T *__restrict__ A, int n, in
     for (int u = 0; u < 8; ++u)
       if (col0 + u < ce)
       {
-        const T *cp = A + (size_t)(col0 + u) * n;
+        const T *cp = A + (size_t)map.g(col0 + u) * n;
 #pragma unroll
         for (int q = 0; q < PER; ++q)
           if (mv[q].x >= 0)
@@ -180,7 +206,7 @@ __global__ void __launch_bounds__(128) lu_mt_kernel(T *__restrict__ A, int n, in
     for (int u = 0; u < 8; ++u)
       if (col0 + u < ce)
       {
-        T *cp = A + (size_t)(col0 + u) * n;
+        T *cp = A + (size_t)map.g(col0 + u) * n;
 #pragma unroll
         for (int q = 0; q < PER; ++q)
           if (mv[q].x >= 0)
@@ -197,7 +223,7 @@ __global__ void __launch_bounds__(128) lu_mt_kernel(T *__restrict__ A, int n, in
     for (int h = 0; h < RL; ++h)
     {
       const int i = lane + 32 * h;
-      x[u][h] = (col0 + u < ce && i < jb) ? A[(size_t)(col0 + u) * n + k0 + i] : T{};
+      x[u][h] = (col0 + u < ce && i < jb) ? A[(size_t)map.g(col0 + u) * n + k0 + i] : T{};
     }
 #pragma unroll 1
   for (int kk = 0; kk < jb; ++kk)
@@ -235,7 +261,7 @@ __global__ void __launch_bounds__(128) lu_mt_kernel(T *__restrict__ A, int n, in
     {
       const int i = lane + 32 * h;
       if (col0 + u < ce && i < jb)
-        A[(size_t)(col0 + u) * n + k0 + i] = x[u][h];
+        A[(size_t)map.g(col0 + u) * n + k0 + i] = x[u][h];
     }
 }
 
@@ -277,7 +303,7 @@ constexpr size_t gemm_smem_bytes()
 // C = A[r0.., cb..ce) for rows >= c0; L21 = A[rows, k0..k0+jb); U12 = A[k0.., cols].
 template <typename T, int NB>
 __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, int k0, int jb,
-                                                      int cb, int ce)
+                                                      int cb, int ce, ColMap map)
 {
   using C = typename CType<T>::type;
   extern __shared__ __align__(16) unsigned char gsm[];
@@ -301,7 +327,7 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
       ta[u] = (kk < jb && row < n) ? to_c(A[(size_t)(k0 + kk) * n + row]) : C(0);
       const int nn = idx / NB, kb = idx % NB;
       const int col = cc0 + nn;
-      tb[u] = (kb < jb && col < ce) ? to_c(A[(size_t)col * n + k0 + kb]) : C(0);
+      tb[u] = (kb < jb && col < ce) ? to_c(A[(size_t)map.g(col) * n + k0 + kb]) : C(0);
     }
 #pragma unroll
     for (int u = 0; u < PT; ++u)
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
     for (int i = 0; i < 8; ++i)
     {
       const int row = r0 + (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
-      acc[i][j] = (row < n && col < ce) ? to_c(A[(size_t)col * n + row]) : C(0);
+      acc[i][j] = (row < n && col < ce) ? to_c(A[(size_t)map.g(col) * n + row]) : C(0);
     }
   }
   __syncthreads();
@@ -355,7 +381,7 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
     {
       const int row = r0 + (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
       if (row < n && col < ce)
-        from_c(A[(size_t)col * n + row], acc[i][j]);
+        from_c(A[(size_t)map.g(col) * n + row], acc[i][j]);
     }
   }
 }
@@ -386,17 +412,37 @@ __global__ void perm_from_ipiv_kernel(const int *__restrict__ ipiv, int n, int *
 }
 
 // ---- host orchestration --------------------------------------------------
-template <typename T, int NB, int RPT>
+__global__ void iota_range_kernel(int *p, int lo, int hi)
+{
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
+    p[i] = i;
+}
+
+// Row-move list of a tall panel from its composed position map pp (rows of
+// [lo, hi) whose content came from another row): new[i] = old[pp[i]].
+__global__ void compact_moves_kernel(const int *__restrict__ pp, int lo, int hi,
+                                     int2 *__restrict__ moves, int *__restrict__ nmoves)
+{
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
+  {
+    const int src = pp[i];
+    if (src != i)
+      moves[atomicAdd(nmoves, 1)] = make_int2(i, src);
+  }
+}
+
+__global__ void min_into_kernel(int *dst, const int *src) { *dst = min(*dst, *src); }
+
+template <typename T, int NB, int RPT, int NTX>
 void configure_panel()
 {
   static bool done = false;
   if (done)
     return;
-  MPIRG_CUDA_CHECK(cudaFuncSetAttribute(panel2::lu_panel2_kernel<T, NB, RPT>,
-                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  MPIRG_CUDA_CHECK(cudaFuncSetAttribute(panel2::lu_panel2_kernel<T, NB, RPT>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)panel2::panel_dyn_smem<T, NB, RPT>()));
+  auto k = panel2::lu_panel2_kernel<T, NB, RPT, NTX>;
+  MPIRG_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  MPIRG_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)panel2::panel_dyn_smem<T, NB, RPT, NTX>()));
   done = true;
 }
 
@@ -412,15 +458,15 @@ void configure_gemm()
   done = true;
 }
 
-template <typename T, int NB, int RPT>
+template <typename T, int NB, int RPT, int NTX = panel2::NT>
 void launch_panel_rpt(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm,
                       DevInfo *info, cudaStream_t s)
 {
-  configure_panel<T, NB, RPT>();
+  configure_panel<T, NB, RPT, NTX>();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs);
-  cfg.blockDim = dim3(panel2::NT);
-  cfg.dynamicSmemBytes = panel2::panel_dyn_smem<T, NB, RPT>();
+  cfg.blockDim = dim3(NTX);
+  cfg.dynamicSmemBytes = panel2::panel_dyn_smem<T, NB, RPT, NTX>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -429,17 +475,37 @@ void launch_panel_rpt(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT>, a, n, k0, jb,
-                                      ipiv, mv, nm, info));
+  MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT, NTX>, a, n, k0,
+                                      jb, ipiv, mv, nm, info));
 }
 
-// Largest rows-per-thread the register file allows for (T, NB).
+// Largest rows-per-thread the shared memory allows for (T, NB) at 256 threads.
 template <typename T, int NB>
 constexpr int max_rpt()
 {
   return panel2::panel_dyn_smem<T, NB, 4>() <= 180 * 1024
              ? 4
              : (panel2::panel_dyn_smem<T, NB, 2>() <= 180 * 1024 ? 2 : 1);
+}
+
+static int panel_max_cs()
+{
+  static const int v = [] {
+    const char *e = std::getenv("MPIRG_PANEL_MAXCS");
+    const int x = e ? std::atoi(e) : panel2::MAXCS;
+    return std::max(1, std::min(panel2::MAXCS, x));
+  }();
+  return v;
+}
+
+// Rows-per-thread for an m-row panel on one cluster at NB (0 = does not fit).
+template <typename T, int NB>
+int panel_rpt(int m)
+{
+  int rpt = 1;
+  while (rpt * panel2::NT * panel_max_cs() < m)
+    rpt *= 2;
+  return rpt <= max_rpt<T, NB>() ? rpt : 0;
 }
 
 template <typename T, int NB, int RPL, int IB>
@@ -544,15 +610,8 @@ void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, Dev
 {
   const int m = n - k0;
   const int per_cta = panel2::NT;
-  static const int max_cs = [] {
-    const char *e = std::getenv("MPIRG_PANEL_MAXCS");
-    const int v = e ? std::atoi(e) : panel2::MAXCS;
-    return std::max(1, std::min(panel2::MAXCS, v));
-  }();
-  int rpt = 1;
-  while (rpt * per_cta * max_cs < m)
-    rpt *= 2;
-  if (rpt > max_rpt<T, NB>())
+  const int rpt = panel_rpt<T, NB>(m);
+  if (rpt == 0)
     throw std::runtime_error("LU panel: n too large for a single-cluster panel at this nb");
   const int cs = std::max(1, (m + rpt * per_cta - 1) / (rpt * per_cta));
   static const bool p5 = [] {
@@ -560,7 +619,7 @@ void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, Dev
     return e && std::atoi(e) == 5;
   }();
   prof_begin(KC_PANEL, s);
-  if (p5 && launch_panel5_dispatch<T, NB>(a, n, k0, jb, ipiv, mv, nm, info, s, max_cs))
+  if (p5 && launch_panel5_dispatch<T, NB>(a, n, k0, jb, ipiv, mv, nm, info, s, panel_max_cs()))
     ;
   else if (rpt == 1)
     launch_panel_rpt<T, NB, 1>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
@@ -577,21 +636,57 @@ void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, Dev
   prof_end(KC_PANEL, s);
 }
 
+// Leaf of a tall panel: 8 columns, 512 threads per CTA, up to 16 CTAs.
+constexpr int LEAF = 8;
+constexpr int LEAF_NT = 512;
+template <typename T>
+constexpr int leaf_max_rpt()
+{
+  return panel2::panel_dyn_smem<T, LEAF, 8, LEAF_NT>() <= 180 * 1024 ? 8 : 4;
+}
+
+template <typename T>
+void launch_leaf(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, DevInfo *info,
+                 cudaStream_t s)
+{
+  const int m = n - k0;
+  int rpt = 1;
+  while (rpt * LEAF_NT * panel_max_cs() < m)
+    rpt *= 2;
+  if (rpt > leaf_max_rpt<T>())
+    throw std::runtime_error("LU panel: n too large for a single-cluster tall panel");
+  const int cs = std::max(1, (m + rpt * LEAF_NT - 1) / (rpt * LEAF_NT));
+  prof_begin(KC_PANEL, s);
+  if (rpt == 1)
+    launch_panel_rpt<T, LEAF, 1, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  else if (rpt == 2)
+    launch_panel_rpt<T, LEAF, 2, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  else if (rpt == 4)
+    launch_panel_rpt<T, LEAF, 4, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  else
+  {
+    if constexpr (leaf_max_rpt<T>() >= 8)
+      launch_panel_rpt<T, LEAF, 8, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  }
+  prof_end(KC_PANEL, s);
+}
+
+// Local column range [cb, ce) of a rank (global ranges when map is the identity).
 template <typename T, int NB>
-void launch_mt(T *a, int n, int k0, int jb, int cb, int ce, const int2 *mv, const int *nm,
-               cudaStream_t s)
+void launch_mt(T *a, int n, int k0, int jb, int cb, int ce, ColMap map, const int2 *mv,
+               const int *nm, cudaStream_t s)
 {
   if (ce <= cb)
     return;
   prof_begin(KC_TRSM, s);
-  lu_mt_kernel<T, NB><<<(ce - cb + MT_COLS - 1) / MT_COLS, 128, 0, s>>>(a, n, k0, jb, cb, ce, mv,
-                                                                      nm);
+  lu_mt_kernel<T, NB><<<(ce - cb + MT_COLS - 1) / MT_COLS, 128, 0, s>>>(a, n, k0, jb, cb, ce,
+                                                                      map, mv, nm);
   MPIRG_CUDA_CHECK(cudaGetLastError());
   prof_end(KC_TRSM, s);
 }
 
 template <typename T, int NB>
-void launch_gemm(T *a, int n, int k0, int jb, int cb, int ce, cudaStream_t s)
+void launch_gemm(T *a, int n, int k0, int jb, int cb, int ce, ColMap map, cudaStream_t s)
 {
   const int c0 = k0 + jb;
   if (ce <= cb || c0 >= n)
@@ -599,14 +694,14 @@ void launch_gemm(T *a, int n, int k0, int jb, int cb, int ce, cudaStream_t s)
   configure_gemm<T, NB>();
   prof_begin(KC_GEMM, s);
   const dim3 grid((n - c0 + GB - 1) / GB, (ce - cb + GB - 1) / GB);
-  lu_gemm_kernel<T, NB><<<grid, 256, gemm_smem_bytes<T, NB>(), s>>>(a, n, k0, jb, cb, ce);
+  lu_gemm_kernel<T, NB><<<grid, 256, gemm_smem_bytes<T, NB>(), s>>>(a, n, k0, jb, cb, ce, map);
   MPIRG_CUDA_CHECK(cudaGetLastError());
   prof_end(KC_GEMM, s);
 }
 
 template <typename T, int NB>
-void launch_moves(T *a, int n, int cb, int ce, const int2 *mv, const int *nm, int *perm,
-                  cudaStream_t s)
+void launch_moves(T *a, int n, int cb, int ce, ColMap map, const int2 *mv, const int *nm,
+                  int *perm, cudaStream_t s)
 {
   const int ncols = ce - cb;
   if (ncols <= 0 && !perm)
@@ -614,14 +709,55 @@ void launch_moves(T *a, int n, int cb, int ce, const int2 *mv, const int *nm, in
   prof_begin(KC_MOVES, s);
   const int warps_needed = std::max(1, (ncols + 3) / 4);
   const int grid = std::max(1, std::min((warps_needed + 7) / 8, 148 * 8));
-  lu_apply_moves_kernel<T, NB><<<grid, 256, 0, s>>>(a, n, cb, std::max(cb, ce), mv, nm, perm);
+  lu_apply_moves_kernel<T, NB><<<grid, 256, 0, s>>>(a, n, cb, std::max(cb, ce), map, mv, nm,
+                                                    perm);
   MPIRG_CUDA_CHECK(cudaGetLastError());
   prof_end(KC_MOVES, s);
+}
+
+// A panel taller than one cluster holds at width NB: factor it as NB/8
+// leaves of 8 columns (the same blocked right-looking order inside the
+// panel: leaf, its moves on the panel's left columns, mt + gemm on the
+// panel's right columns), composing the leaves' row moves in pp.
+template <typename T, int NB>
+void panel_tall(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, LuWorkspace &ws,
+                DevInfo *info, cudaStream_t s)
+{
+  const ColMap id{};
+  const int m = n - k0;
+  const int g = std::min(148 * 4, (m + 255) / 256);
+  iota_range_kernel<<<g, 256, 0, s>>>(ws.pp, k0, n);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+  const int nleaf = (jb + LEAF - 1) / LEAF;
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(ws.snm, 0, sizeof(int) * nleaf, s));
+  for (int l = 0; l < nleaf; ++l)
+  {
+    const int ks = k0 + l * LEAF, w = std::min(LEAF, jb - l * LEAF);
+    int2 *smv = ws.smv + (size_t)l * 2 * LEAF;
+    int *snm = ws.snm + l;
+    launch_leaf<T>(a, n, ks, w, ipiv, smv, snm, info, s);
+    launch_moves<T, LEAF>(a, n, k0, ks, id, smv, snm, ws.pp, s);
+    launch_mt<T, LEAF>(a, n, ks, w, ks + w, k0 + jb, id, smv, snm, s);
+    launch_gemm<T, LEAF>(a, n, ks, w, ks + w, k0 + jb, id, s);
+  }
+  compact_moves_kernel<<<g, 256, 0, s>>>(ws.pp, k0, n, mv, nm);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+template <typename T, int NB>
+void panel_any(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, LuWorkspace &ws,
+               DevInfo *info, cudaStream_t s)
+{
+  if (panel_rpt<T, NB>(n - k0) > 0)
+    launch_panel<T, NB>(a, n, k0, jb, ipiv, mv, nm, info, s);
+  else
+    panel_tall<T, NB>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
 }
 
 template <typename T, int NB>
 void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, cudaStream_t s)
 {
+  const ColMap id{};
   cudaStream_t side = static_cast<cudaStream_t>(ws.side);
   cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);  // [3][npanels]: P, N, R
   const int np = ws.npanels;
@@ -642,28 +778,86 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
     int *nm = ws.nmoves + p;
     cudaEvent_t evP = ev[p], evN = ev[np + p], evR = ev[2 * np + p];
     // main: the critical chain
-    launch_panel<T, NB>(a, n, k0, jb, ipiv, mv, nm, info, s);
+    panel_any<T, NB>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
     MPIRG_CUDA_CHECK(cudaEventRecord(evP, s));
     const int cnext = std::min(n, c0 + NB);
     if (c0 < n)
     {
       if (p > 0)
         MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + p - 1], 0));
-      launch_mt<T, NB>(a, n, k0, jb, c0, cnext, mv, nm, s);
-      launch_gemm<T, NB>(a, n, k0, jb, c0, cnext, s);
+      launch_mt<T, NB>(a, n, k0, jb, c0, cnext, id, mv, nm, s);
+      launch_gemm<T, NB>(a, n, k0, jb, c0, cnext, id, s);
     }
     MPIRG_CUDA_CHECK(cudaEventRecord(evN, s));
     // side: the rest of this step's update + the left-column moves
     MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, evP, 0));
     if (cnext < n)
     {
-      launch_mt<T, NB>(a, n, k0, jb, cnext, n, mv, nm, side);
-      launch_gemm<T, NB>(a, n, k0, jb, cnext, n, side);
+      launch_mt<T, NB>(a, n, k0, jb, cnext, n, id, mv, nm, side);
+      launch_gemm<T, NB>(a, n, k0, jb, cnext, n, id, side);
     }
-    launch_moves<T, NB>(a, n, 0, k0, mv, nm, perm, side);
+    launch_moves<T, NB>(a, n, 0, k0, id, mv, nm, perm, side);
     MPIRG_CUDA_CHECK(cudaEventRecord(evR, side));
   }
   MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + np - 1], 0));
+}
+
+// ---- one rank of the 1-D block-cyclic LU (config 5a) ----------------------
+// Step p (k0 = p*nb): the owner of column block p factors the panel
+// (dlu_panel); the panel rows [k0, n), its pivots and its row moves go to
+// every rank (the caller's broadcast); every rank then applies the moves,
+// U12 = L11^-1 A12 and A22 -= L21 U12 to the columns it owns (dlu_update).
+// part 1 (NEXT) updates only the next panel's columns when this rank owns
+// them (look-ahead on the caller's stream); part 2 (REST) the remaining
+// owned columns + the left-column moves on the side stream; part 0 both.
+template <typename T, int NB>
+void dlu_update_t(DluPlan &d, T *a, int p, int part, int *perm, cudaStream_t s)
+{
+  LuWorkspace &ws = d.ws;
+  const ColMap map{d.G, d.r, d.sh};
+  const int n = d.n, np = ws.npanels;
+  const int k0 = p * NB, jb = std::min(NB, n - k0), c0 = k0 + jb;
+  const int cnext = std::min(n, c0 + NB);
+  // [c0, cnext) lies in one distribution block (block_cols is a multiple of nb)
+  const bool nextmine = p + 1 < np && ((c0 >> d.sh) % d.G) == d.r;
+  const int2 *mv = ws.moves + (size_t)p * 2 * NB;
+  const int *nm = ws.nmoves + p;
+  cudaStream_t side = static_cast<cudaStream_t>(ws.side);
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);
+  const int Lc0 = map.lcount(c0), Lcn = map.lcount(cnext), Ln = map.lcount(n);
+  if (part == 0 || part == 1)
+  {
+    if (nextmine)
+    {
+      if (part == 1 && p > 0)
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + p - 1], 0));
+      launch_mt<T, NB>(a, n, k0, jb, Lc0, Lcn, map, mv, nm, s);
+      launch_gemm<T, NB>(a, n, k0, jb, Lc0, Lcn, map, s);
+    }
+  }
+  if (part == 0 || part == 2)
+  {
+    cudaStream_t t = part == 0 ? s : side;
+    if (part == 2)
+    {
+      MPIRG_CUDA_CHECK(cudaEventRecord(ev[p], s));
+      MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, ev[p], 0));
+    }
+    const int Lb = nextmine ? Lcn : Lc0;
+    launch_mt<T, NB>(a, n, k0, jb, Lb, Ln, map, mv, nm, t);
+    launch_gemm<T, NB>(a, n, k0, jb, Lb, Ln, map, t);
+    launch_moves<T, NB>(a, n, 0, map.lcount(k0), map, mv, nm, perm, t);
+    if (part == 2)
+      MPIRG_CUDA_CHECK(cudaEventRecord(ev[2 * np + p], side));
+  }
+}
+
+template <typename T, int NB>
+void dlu_panel_t(DluPlan &d, T *a, int p, int *ipiv, DevInfo *info, cudaStream_t s)
+{
+  const int k0 = p * NB, jb = std::min(NB, d.n - k0);
+  panel_any<T, NB>(a, d.n, k0, jb, ipiv, d.ws.moves + (size_t)p * 2 * NB, d.ws.nmoves + p,
+                   d.ws, info, s);
 }
 
 }  // namespace
@@ -685,6 +879,9 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   ws.npanels = std::max(1, (n + ws.nb - 1) / ws.nb);
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.moves, sizeof(int2) * (size_t)ws.npanels * 2 * ws.nb));
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.nmoves, sizeof(int) * (size_t)ws.npanels));
+  MPIRG_CUDA_CHECK(cudaMalloc(&ws.pp, sizeof(int) * (size_t)std::max(1, n)));
+  MPIRG_CUDA_CHECK(cudaMalloc(&ws.smv, sizeof(int2) * 2 * (size_t)ws.nb));
+  MPIRG_CUDA_CHECK(cudaMalloc(&ws.snm, sizeof(int) * (size_t)ws.nb));
   cudaStream_t side;
   MPIRG_CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   ws.side = side;
@@ -696,10 +893,10 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
 
 void lu_workspace_free(LuWorkspace &ws)
 {
-  if (ws.moves)
-    cudaFree(ws.moves);
-  if (ws.nmoves)
-    cudaFree(ws.nmoves);
+  for (void *p : {(void *)ws.moves, (void *)ws.nmoves, (void *)ws.pp, (void *)ws.smv,
+                  (void *)ws.snm})
+    if (p)
+      cudaFree(p);
   if (ws.events)
   {
     auto *ev = static_cast<cudaEvent_t *>(ws.events);
@@ -741,6 +938,85 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
 void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s)
 {
   perm_from_ipiv_kernel<<<1, 32, 0, s>>>(ipiv, n, perm);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+// ---- distributed (per-rank) driver -----------------------------------------
+void dlu_alloc(DluPlan &d, int prec, int n, int nb, int G, int r, int block_cols)
+{
+  d.prec = prec;
+  d.n = n;
+  d.G = G;
+  d.r = r;
+  int sh = 0;
+  while ((1 << sh) < block_cols)
+    ++sh;
+  d.sh = sh;
+  lu_workspace_alloc(d.ws, prec, n, nb);
+}
+
+void dlu_free(DluPlan &d) { lu_workspace_free(d.ws); }
+
+void dlu_begin(DluPlan &d, int *perm, cudaStream_t s)
+{
+  if (perm)
+  {
+    iota_kernel<<<(d.n + 255) / 256, 256, 0, s>>>(perm, d.n);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  }
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(d.ws.nmoves, 0, sizeof(int) * d.ws.npanels, s));
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(d.ws.events);
+  MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(static_cast<cudaStream_t>(d.ws.side), ev[0], 0));
+}
+
+template <typename F>
+static void dlu_dispatch(const DluPlan &d, F &&f)
+{
+  const int nb = d.ws.nb;
+  auto go = [&](auto tag) {
+    using T = typename decltype(tag)::type;
+    if (nb == 64)
+      f.template operator()<T, 64>();
+    else if (nb == 32)
+      f.template operator()<T, 32>();
+    else
+      f.template operator()<T, 16>();
+  };
+  if (d.prec == B64)
+    go(std::type_identity<double>{});
+  else if (d.prec == B32)
+    go(std::type_identity<float>{});
+  else
+    go(std::type_identity<h16>{});
+}
+
+void dlu_panel(DluPlan &d, void *a, int p, int *ipiv, DevInfo *info, cudaStream_t s)
+{
+  dlu_dispatch(d, [&]<typename T, int NB>() {
+    dlu_panel_t<T, NB>(d, static_cast<T *>(a), p, ipiv, info, s);
+  });
+}
+
+void dlu_update(DluPlan &d, void *a, int p, int part, int *perm, cudaStream_t s)
+{
+  dlu_dispatch(d, [&]<typename T, int NB>() {
+    dlu_update_t<T, NB>(d, static_cast<T *>(a), p, part, perm, s);
+  });
+}
+
+void dlu_end(DluPlan &d, cudaStream_t s)
+{
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(d.ws.events);
+  const int np = d.ws.npanels;
+  // every REST event that was recorded (part 2 calls) is before the last one
+  MPIRG_CUDA_CHECK(cudaEventRecord(ev[np + np - 1], static_cast<cudaStream_t>(d.ws.side)));
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[np + np - 1], 0));
+}
+
+void dlu_merge_singular(int *dst, const int *src, cudaStream_t s)
+{
+  min_into_kernel<<<1, 1, 0, s>>>(dst, src);
   MPIRG_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -209,10 +209,10 @@ __device__ __forceinline__ uint32_t cluster_size()
 __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Dynamic shared memory: P[NB][R] (this CTA's rows, column-major) + Ub[IB][NB].
-template <typename T, int NB, int RPT>
+template <typename T, int NB, int RPT, int NTX = NT>
 __host__ __device__ constexpr size_t panel_dyn_smem()
 {
-  return a16(sizeof(T) * (size_t)NB * RPT * NT) + a16(sizeof(T) * (size_t)IB * NB);
+  return a16(sizeof(T) * (size_t)NB * RPT * NTX) + a16(sizeof(T) * (size_t)IB * NB);
 }
 
 #ifdef MPIRG_DEBUG_PANEL
@@ -234,11 +234,16 @@ __host__ __device__ constexpr size_t panel_dyn_smem()
 #endif
 
 // rows of this CTA: row0 + t + q*NT, q < RPT (R = RPT*NT rows per CTA)
-template <typename T, int NB, int RPT>
-__global__ void __launch_bounds__(NT, 1)
+// NTX threads per CTA (256 for the panel of the blocked LU; 512 for the
+// 8-column leaf of a tall panel, lu.cu panel_tall).
+template <typename T, int NB, int RPT, int NTX = NT>
+__global__ void __launch_bounds__(NTX, 1)
     lu_panel2_kernel(T *__restrict__ A, int n, int k0, int jb, int *__restrict__ ipiv,
                      int2 *__restrict__ moves, int *__restrict__ nmoves, DevInfo *info)
 {
+  constexpr int NT = NTX;  // hides the namespace default inside this kernel
+  constexpr int NW = NTX / 32;
+  static_assert(NW <= 32 && NW * 2 >= MAXCS, "push mapping needs 2*NW >= MAXCS");
   using S = Slot<T, NB>;
   constexpr int R = RPT * NT;
   constexpr bool WIDE = sizeof(T) > 4;

@@ -256,15 +256,18 @@ struct mpirg_factorization
       cudaStreamDestroy(stream);
   }
 
-  // MPFactorization::refactor (mp_structures.hpp:155-169).
-  void refactor()
+  // MPFactorization::refactor (mp_structures.hpp:155-169). do_lu = false
+  // stops after the interprecision copy (the distributed LU of config 5a
+  // factors a_low itself, then calls set_factored).
+  void refactor(bool do_lu = true)
   {
     cudaStream_t s = stream;
     MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
     reset_info(info, s);
     MPIRG_CUDA_CHECK(cudaMemsetAsync(scal, 0, sizeof(unsigned long long), s));
     launch_cast_norm(cfg.tw, cfg.tf, n, n, a_high, a_low, scal, info, s);
-    launch_lu(cfg.tf, cfg.lu_mode, a_low, n, ipiv, perm, luws, info, s);
+    if (do_lu)
+      launch_lu(cfg.tf, cfg.lu_mode, a_low, n, ipiv, perm, luws, info, s);
     MPIRG_CUDA_CHECK(cudaEventRecord(ev[1], s));
     MPIRG_CUDA_CHECK(cudaMemcpyAsync(h_info, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
     MPIRG_CUDA_CHECK(
@@ -290,7 +293,7 @@ struct mpirg_factorization
                          prec_name(cfg.tf) + " value",
                      -1, v};
     }
-    if (h_info->singular_col != INT_MAX)
+    if (do_lu && h_info->singular_col != INT_MAX)
       throw ApiError{MPIRG_ERR_SINGULAR, "pivot column is exactly zero", h_info->singular_col};
   }
 
@@ -1044,3 +1047,241 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
 }
 
 }  // extern "C"
+
+
+// ---------------------------------------------------------------------------
+// Externally factored handles + the per-rank distributed LU (config 5a)
+// ---------------------------------------------------------------------------
+int mpirg_factorization_cast(mpirg_factorization *f, const void *a, int a_on_device,
+                             mpirg_error *err)
+{
+  return guarded(err, [&] {
+    MPIRG_CUDA_CHECK(cudaSetDevice(f->device));
+    if (a)
+      MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->a_high, a, (size_t)f->n * f->n * f->tw_bytes(),
+                                       a_on_device ? cudaMemcpyDeviceToDevice
+                                                   : cudaMemcpyHostToDevice,
+                                       f->stream));
+    if (f->n > 0)
+      f->refactor(false);
+  });
+}
+
+int mpirg_factorization_buffers(mpirg_factorization *f, void **a_low, int **ipiv, int **perm,
+                                void **stream)
+{
+  if (a_low)
+    *a_low = f->a_low;
+  if (ipiv)
+    *ipiv = f->ipiv;
+  if (perm)
+    *perm = f->perm;
+  if (stream)
+    *stream = f->stream;
+  return MPIRG_OK;
+}
+
+int mpirg_factorization_set_factored(mpirg_factorization *f, int singular_col, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    if (singular_col >= 0 && singular_col < f->n)
+      throw ApiError{MPIRG_ERR_SINGULAR, "pivot column is exactly zero", singular_col};
+  });
+}
+
+struct mpirg_dlu
+{
+  DluPlan plan;
+  int device = 0;
+  int nb = 0, np = 0, block_cols = 0;
+  DevInfo *info = nullptr;
+  int *hdr = nullptr;  // scratch for a received header
+};
+
+namespace
+{
+size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+struct MsgLayout
+{
+  size_t ipiv, moves, panel, total;
+};
+MsgLayout msg_layout(const mpirg_dlu *h, int p)
+{
+  const int n = h->plan.n, k0 = p * h->nb, jb = std::min(h->nb, n - k0);
+  MsgLayout m;
+  m.ipiv = 16;
+  m.moves = al16(m.ipiv + sizeof(int) * (size_t)jb);
+  m.panel = al16(m.moves + sizeof(int2) * 2 * (size_t)h->nb);
+  m.total = al16(m.panel + elem_size(h->plan.prec) * (size_t)(n - k0) * jb);
+  return m;
+}
+void check_step(const mpirg_dlu *h, int p)
+{
+  if (p < 0 || p >= h->np)
+    throw ApiError{MPIRG_ERR_INVALID_PARAM, "panel index out of range"};
+}
+}  // namespace
+
+int mpirg_dlu_create(mpirg_dlu **out, int prec, int n, int nb, int nranks, int rank,
+                     int block_cols, int device, mpirg_error *err)
+{
+  *out = nullptr;
+  return guarded(err, [&] {
+    if (n <= 0)
+      throw ApiError{MPIRG_ERR_INVALID_SIZE, "distributed LU needs n > 0"};
+    if (prec != B64 && prec != B32 && prec != B16)
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG, "unknown factor precision"};
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "rank must lie in [0, nranks)"};
+    require_gpu();
+    if (device >= 0)
+      MPIRG_CUDA_CHECK(cudaSetDevice(device));
+    const int b = lu_choose_nb(prec, n, nb);
+    int bc = block_cols > 0 ? block_cols : std::max(256, b);
+    if ((bc & (bc - 1)) != 0 || bc % b != 0)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM,
+                     "block_cols must be a power of two and a multiple of nb"};
+    auto *h = new mpirg_dlu;
+    try
+    {
+      MPIRG_CUDA_CHECK(cudaGetDevice(&h->device));
+      dlu_alloc(h->plan, prec, n, b, nranks, rank, bc);
+      h->nb = b;
+      h->np = h->plan.ws.npanels;
+      h->block_cols = bc;
+      h->info = dalloc<DevInfo>(1);
+      h->hdr = dalloc<int>(4);
+    }
+    catch (...)
+    {
+      dlu_free(h->plan);
+      if (h->info)
+        cudaFree(h->info);
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void mpirg_dlu_destroy(mpirg_dlu *h)
+{
+  if (!h)
+    return;
+  cudaSetDevice(h->device);
+  dlu_free(h->plan);
+  if (h->info)
+    cudaFree(h->info);
+  if (h->hdr)
+    cudaFree(h->hdr);
+  delete h;
+}
+
+int mpirg_dlu_nb(const mpirg_dlu *h) { return h->nb; }
+int mpirg_dlu_npanels(const mpirg_dlu *h) { return h->np; }
+int mpirg_dlu_block_cols(const mpirg_dlu *h) { return h->block_cols; }
+int mpirg_dlu_owner(const mpirg_dlu *h, int p)
+{
+  return ((p * h->nb) / h->block_cols) % h->plan.G;
+}
+size_t mpirg_dlu_msg_bytes(const mpirg_dlu *h, int p) { return msg_layout(h, p).total; }
+
+int mpirg_dlu_begin(mpirg_dlu *h, int *perm, void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
+    auto s = static_cast<cudaStream_t>(stream);
+    reset_info(h->info, s);
+    dlu_begin(h->plan, perm, s);
+  });
+}
+
+int mpirg_dlu_panel(mpirg_dlu *h, void *a, int p, int *ipiv, void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    check_step(h, p);
+    if (mpirg_dlu_owner(h, p) != h->plan.r)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "this rank does not own the panel"};
+    MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
+    dlu_panel(h->plan, a, p, ipiv, h->info, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// Step message: [nmoves, singular_col | ipiv[jb] | moves[2 nb] | panel rows k0..n-1 x jb].
+int mpirg_dlu_pack(mpirg_dlu *h, const void *a, int p, const int *ipiv, void *msg,
+                   void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    check_step(h, p);
+    MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
+    auto s = static_cast<cudaStream_t>(stream);
+    const MsgLayout L = msg_layout(h, p);
+    const int n = h->plan.n, k0 = p * h->nb, jb = std::min(h->nb, n - k0);
+    const size_t es = elem_size(h->plan.prec);
+    char *m = static_cast<char *>(msg);
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m, h->plan.ws.nmoves + p, sizeof(int),
+                                     cudaMemcpyDeviceToDevice, s));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + 4, &h->info->singular_col, sizeof(int),
+                                     cudaMemcpyDeviceToDevice, s));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + L.ipiv, ipiv + k0, sizeof(int) * jb,
+                                     cudaMemcpyDeviceToDevice, s));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + L.moves, h->plan.ws.moves + (size_t)p * 2 * h->nb,
+                                     sizeof(int2) * 2 * h->nb, cudaMemcpyDeviceToDevice, s));
+    MPIRG_CUDA_CHECK(cudaMemcpy2DAsync(m + L.panel, (n - k0) * es,
+                                       static_cast<const char *>(a) + ((size_t)k0 * n + k0) * es,
+                                       (size_t)n * es, (n - k0) * es, jb,
+                                       cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+int mpirg_dlu_unpack(mpirg_dlu *h, void *a, int p, int *ipiv, const void *msg, void *stream,
+                     mpirg_error *err)
+{
+  return guarded(err, [&] {
+    check_step(h, p);
+    MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
+    auto s = static_cast<cudaStream_t>(stream);
+    const MsgLayout L = msg_layout(h, p);
+    const int n = h->plan.n, k0 = p * h->nb, jb = std::min(h->nb, n - k0);
+    const size_t es = elem_size(h->plan.prec);
+    const char *m = static_cast<const char *>(msg);
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->plan.ws.nmoves + p, m, sizeof(int),
+                                     cudaMemcpyDeviceToDevice, s));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->hdr, m + 4, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    dlu_merge_singular(&h->info->singular_col, h->hdr, s);
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(ipiv + k0, m + L.ipiv, sizeof(int) * jb,
+                                     cudaMemcpyDeviceToDevice, s));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->plan.ws.moves + (size_t)p * 2 * h->nb, m + L.moves,
+                                     sizeof(int2) * 2 * h->nb, cudaMemcpyDeviceToDevice, s));
+    MPIRG_CUDA_CHECK(cudaMemcpy2DAsync(static_cast<char *>(a) + ((size_t)k0 * n + k0) * es,
+                                       (size_t)n * es, m + L.panel, (n - k0) * es,
+                                       (n - k0) * es, jb, cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+int mpirg_dlu_update(mpirg_dlu *h, void *a, int p, int part, int *perm, void *stream,
+                     mpirg_error *err)
+{
+  return guarded(err, [&] {
+    check_step(h, p);
+    if (part < 0 || part > 2)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "part must be 0, 1 or 2"};
+    MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
+    dlu_update(h->plan, a, p, part, perm, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mpirg_dlu_end(mpirg_dlu *h, void *stream, int *singular_col, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
+    auto s = static_cast<cudaStream_t>(stream);
+    dlu_end(h->plan, s);
+    int sc = INT_MAX;
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(&sc, &h->info->singular_col, sizeof(int),
+                                     cudaMemcpyDeviceToHost, s));
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (singular_col)
+      *singular_col = sc == INT_MAX ? -1 : sc;
+  });
+}

@@ -145,6 +145,21 @@ class Factorization:
         L.check(st, err)
         L.lib().mpirg_factorization_config(self._h, C.byref(self._cfg))
 
+    @classmethod
+    def _allocate(cls, n: int, cfg) -> "Factorization":
+        """A handle with buffers but no factorization yet (the distributed LU
+        of config 5a fills it: mpirg_factorization_cast / _set_factored)."""
+        self = cls.__new__(cls)
+        self._n = n
+        self._cfg = cfg
+        self._h = C.c_void_p()
+        err = L.mpirg_error()
+        st = L.lib().mpirg_factorization_create(C.byref(self._h), n, C.byref(cfg), None, 1,
+                                                C.byref(err))
+        L.check(st, err)
+        L.lib().mpirg_factorization_config(self._h, C.byref(self._cfg))
+        return self
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
