@@ -1,6 +1,9 @@
 #!/usr/bin/env python
 """bench.py -- IR time-to-solution on B200 (BASELINE.json configs[1], config 2a).
 
+(--config cfg1|cfg2b|cfg3|cfg4 [--lu-mode tc] measures the other BASELINE
+configs the same way; the default line is config 2a.)
+
 Workload (one "step"): the reference's factor-once + refine path on
 A = I - 800 G (N = 4096, trapezoid Green's operator, fp64), b ~ N(0,1) seed 0,
 <TW,TF,TR> = <fp64, fp32, fp64>, scaled (LPS) corrections, backward-error
@@ -32,9 +35,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_DEFAULT = 4096
-ALPHA = 800.0
-CE, LITMAX = 10.0, 20
+PREC = {0: "f64", 1: "f32", 2: "f16"}
+ESZ = {0: 8, 1: 4, 2: 2}
 METRIC = "IR time-to-solution & LU GFLOP/s (2N^3/3) vs fp16-TC/fp32 peak"
 HBM_FALLBACK = 6650.0
 
@@ -45,22 +47,33 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--config", default="cfg2a",
+                    choices=["cfg1", "cfg2a", "cfg2b", "cfg3", "cfg4"],
+                    help="BASELINE config (default cfg2a = the headline workload)")
+    ap.add_argument("--lu-mode", default="exact", choices=["exact", "tc"],
+                    help="tc: tcgen05 trailing update for binary16 factors (cfg3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
-def inputs(n):
-    """Seeded host inputs shared by every arm (cfg 2a)."""
+def workload(args):
+    """Seeded host inputs + reference parameters; default cfg 2a."""
+    from paper_2311_14616_b200 import configs
+    cfg = configs.config(args.config, args.n)
+    n = cfg["n"]
+    tag = (f"{args.config}: N={n}, <{PREC[cfg['tw']]},{PREC[cfg['tf']]},{PREC[cfg['tr']]}>, "
+           f"ce={cfg['ce']}, litmax={cfg['litmax']}"
+           + (", lu_mode=tc (tcgen05 trailing update)" if args.lu_mode == "tc" else ""))
+    cfg["workload"] = tag
+    return cfg
+
+
+def to_tw(arr64, tw):
+    """The facade's one rounding of float64 inputs into TW (runtime.cpp:23-28)."""
     import numpy as np
-    from paper_2311_14616_b200 import lib
-    L = lib()
-    a = np.empty(n * n, dtype=np.float64)  # column-major storage
-    L.mpirg_gen_greens_operator(n, ALPHA, a.ctypes.data)
-    b = np.empty(n, dtype=np.float64)
-    L.mpirg_gen_normal_matrix(n, 1, 0, b.ctypes.data)
-    return a, b
+    return arr64 if tw == 0 else arr64.astype(np.float32)
 
 
 def measured_peaks():
@@ -164,18 +177,21 @@ def run_reference(args, world, rank):
         return
     import numpy as np
     import oracle
-    n = args.n
-    a, b = inputs(n)
+    cfg = workload(args)
+    n = cfg["n"]
+    a, b = cfg["a"], cfg["b"]
     impl = oracle.reference()
     kind = "reference"
     if impl is None:
         impl, kind = oracle.restatement(), "port"
-    af = a.reshape(n, n).T  # column-major storage viewed as an (n, n) matrix
+    af = to_tw(a, cfg["tw"]).reshape(n, n).T  # column-major storage viewed as (n, n)
+    bw = to_tw(b, cfg["tw"])
     times = []
     last = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        last = impl.ir(0, 1, 0, af, b, resid_term=False, ce=CE, litmax=LITMAX)
+        last = impl.ir(cfg["tw"], cfg["tf"], cfg["tr"], af, bw, on_the_fly=cfg["on_the_fly"],
+                       resid_term=cfg["resid_term"], ce=cfg["ce"], litmax=cfg["litmax"])
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -183,13 +199,14 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": sec, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32",
-        "data": "synthetic (seeded: Green's operator, libstdc++ mt19937_64 normal b)",
-        "config": {"workload": f"cfg2a: I-800G N={n}, <f64,f32,f64> LPS, ce={CE}, "
-                               f"litmax={LITMAX}", "n": n},
-        "cpu_baseline": {"value": sec, "unit": "s", "cores": 1, "kind": kind,
-                         "sample": f"full cfg2a solve (refactor + IR) at N={n}, "
-                                   "fp32 LU single-threaded per mp_structures.hpp:166-167"},
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": f"{PREC[cfg['tw']]}/{PREC[cfg['tf']]}",
+        "data": "synthetic (seeded: libstdc++ mt19937_64 generators, SURVEY 8(d))",
+        "config": {"workload": cfg["workload"], "n": n},
+        "cpu_baseline": {"value": sec, "unit": "s",
+                         "cores": 1 if cfg["tf"] != 2 else os.cpu_count(), "kind": kind,
+                         "sample": f"full {args.config} solve (refactor + IR) at N={n}; fp32 "
+                                   "LU single-threaded per mp_structures.hpp:166-167"},
         "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_split_s": {"factor": last["t_factor"], "solve": last["t_solve"]},
         "iters": len(last["rhist"]) - 1, "reason": last["reason"],
@@ -220,20 +237,23 @@ def run_ours(args, world, rank, local):
     from paper_2311_14616_b200 import _lib as L
     lib = L.lib()
     torch.cuda.set_device(local)
-    n = args.n
-    a_host, b_host = inputs(n)
-
-    cfg = L.mpirg_config(0, 1, 0, -1, 0, L.LU_EXACT, 0, local)
-    tp = L.mpirg_term_params(1.0, CE, 0.5, LITMAX)
+    wl = workload(args)
+    n = wl["n"]
+    tw, tf, tr = wl["tw"], wl["tf"], wl["tr"]
+    a_host, b_host = to_tw(wl["a"], tw), to_tw(wl["b"], tw)
+    litmax = wl["litmax"]
+    cfg = L.mpirg_config(tw, tf, tr, wl["on_the_fly"], int(wl["resid_term"]),
+                         L.LU_TC if args.lu_mode == "tc" else L.LU_EXACT, 0, local)
+    tp = L.mpirg_term_params(1.0, wl["ce"], 0.5, litmax)
     a_dev = torch.from_numpy(a_host).cuda()
     b_dev = torch.from_numpy(b_host).cuda()
-    sol_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    sol_dev = torch.empty(n, dtype=b_dev.dtype, device="cuda")
     h = C.c_void_p()
     err = L.mpirg_error()
     L.check(lib.mpirg_factorization_create(C.byref(h), n, C.byref(cfg), a_dev.data_ptr(), 1,
                                            C.byref(err)), err)
     lib.mpirg_factorization_config(h, C.byref(cfg))
-    cap = LITMAX + 1
+    cap = litmax + 1
     rh, dh = (C.c_double * cap)(), (C.c_double * cap)()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -286,7 +306,7 @@ def run_ours(args, world, rank, local):
     if not args.no_e2e:
         a_pin = torch.from_numpy(a_host).pin_memory()
         b_pin = torch.from_numpy(b_host).pin_memory()
-        x_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+        x_pin = torch.empty(n, dtype=b_dev.dtype).pin_memory()
         e2e_t = []
         for i in range(max(1, args.warmup // 2) + args.steps):
             flush.fill_(1.0)
@@ -300,8 +320,8 @@ def run_ours(args, world, rank, local):
             if i >= max(1, args.warmup // 2):
                 e2e_t.append(dt)
         e2e_s = max_over_ranks(statistics.mean(e2e_t), world)
-        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": n * n * 8 + n * 8,
-               "d2h_bytes_per_step": n * 8 + 3 * 8 * cap}
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": (n * n + n) * ESZ[tw],
+               "d2h_bytes_per_step": n * ESZ[tw] + 3 * 8 * cap}
 
     # Roofline of the dominant kernel class.
     peaks, peak_src = measured_peaks()
@@ -309,9 +329,14 @@ def run_ours(args, world, rank, local):
     ffma = C.c_double(0.0)
     ffma_ms = C.c_double(0.0)
     lib.mpirg_ffma_peak(C.byref(ffma), C.byref(ffma_ms))
-    nb = 64 if n <= 8192 else 32
+    nb = (64 if n <= 4096 else (32 if n <= 8192 else 16)) if tf == 0 else \
+        (64 if n <= 8192 else 32)
     work = lu_work(n, nb)
-    tf_b, tw_b = 4, 8
+    tf_b, tw_b = ESZ[tf], ESZ[tw]
+    tc = args.lu_mode == "tc" and tf == 2
+    gemm_bound = ("tcgen05 fp16 (fp32 accumulate)" if tc else
+                  {0: "fp64 SIMT", 1: "fp32-ffma", 2: "fp16 SIMT (two roundings per term)"}[tf])
+    gemm_peak = float(peaks.get("bf16_tflops", 0.0)) if tc else ffma.value
     kernels = {}
     for name in L.KERNEL_CLASSES:
         kms = kernel_ms[name]
@@ -320,8 +345,8 @@ def run_ours(args, world, rank, local):
         d = {"ms_per_step": kms, "launches_per_step": kernel_n[name],
              "share_of_step": kms / mean_ms}
         if name == "gemm":
-            d.update(bound="fp32-ffma", achieved=work["gemm"] / (kms * 1e-3) / 1e12,
-                     unit="TFLOP/s", peak=ffma.value)
+            d.update(bound=gemm_bound, achieved=work["gemm"] / (kms * 1e-3) / 1e12,
+                     unit="TFLOP/s", peak=gemm_peak)
         elif name == "panel":
             d.update(bound="latency (one pivot search per column)", unit="TFLOP/s",
                      achieved=work["panel"] / (kms * 1e-3) / 1e12, peak=ffma.value)
@@ -345,18 +370,21 @@ def run_ours(args, world, rank, local):
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
     roof_bound = "hbm" if dk.get("bound") == "hbm" else "tensor"
+    peak_note = ("MEASURED_PEAKS.json hbm_gbs" if dk.get("unit") == "GB/s" else
+                 "MEASURED_PEAKS.json bf16_tflops (tcgen05 kind::f16 rate)"
+                 if (dom == "gemm" and tc) else
+                 "fp32 FFMA microbenchmark (mpirg_ffma_peak) on this GPU; TF32/tensor cores "
+                 "excluded by contract")
     roofline = {"kernel": dom, "bound": roof_bound, "bound_detail": dk.get("bound"),
                 "achieved": dk.get("achieved"), "peak": dk.get("peak"), "unit": dk.get("unit"),
                 "frac": dk.get("frac"), "traffic": None,
-                "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if dk.get("unit") == "GB/s"
-                                else "fp32 FFMA microbenchmark (mpirg_ffma_peak) on this GPU; "
-                                     "TF32/tensor cores excluded by contract"),
+                "peak_source": peak_note,
                 "peak_kind": peak_src}
     lu_ms = sum(kernel_ms[k] for k in ("panel", "moves", "trsm", "gemm"))
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(n, a_host, b_host)
+        cpu = cpu_baseline(args, wl, a_host, b_host)
 
     if rank == 0:
         launches = int(round(sum(kernel_n.values())))
@@ -364,10 +392,9 @@ def run_ours(args, world, rank, local):
             "metric": METRIC, "value": mean_ms / 1e3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64/f32 (TW=fp64, TF=fp32, TR=fp64)",
-            "data": "synthetic (seeded: Green's operator I-800G, libstdc++ mt19937_64 normal b)",
-            "config": {"workload": f"cfg2a: I-800G N={n}, <f64,f32,f64> LPS, ce={CE}, "
-                                   f"litmax={LITMAX}", "n": n, "nb": nb,
+            "dtype": f"{PREC[tw]}/{PREC[tf]} (TW={PREC[tw]}, TF={PREC[tf]}, TR={PREC[tr]})",
+            "data": "synthetic (seeded: libstdc++ mt19937_64 generators per SURVEY 8(d))",
+            "config": {"workload": wl["workload"], "n": n, "nb": nb,
                        "parallelism": "replicas" if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write), flush excluded",
                        "a_resident_in_hbm": True},
@@ -385,8 +412,9 @@ def run_ours(args, world, rank, local):
     lib.mpirg_factorization_destroy(h)
 
 
-def cpu_baseline(n, a_host, b_host):
-    """The compiled reference (oracle/_ref) on this host: one full cfg2a solve."""
+def cpu_baseline(args, wl, a_host, b_host):
+    """The compiled reference (oracle/_ref) on this host: one full solve."""
+    n = wl["n"]
     try:
         import oracle
         impl = oracle.reference()
@@ -395,10 +423,12 @@ def cpu_baseline(n, a_host, b_host):
             impl, kind = oracle.restatement(), "port"
         af = a_host.reshape(n, n).T
         t0 = time.perf_counter()
-        rep = impl.ir(0, 1, 0, af, b_host, resid_term=False, ce=CE, litmax=LITMAX)
+        rep = impl.ir(wl["tw"], wl["tf"], wl["tr"], af, b_host, on_the_fly=wl["on_the_fly"],
+                      resid_term=wl["resid_term"], ce=wl["ce"], litmax=wl["litmax"])
         dt = time.perf_counter() - t0
-        return {"value": dt, "unit": "s", "cores": 1, "kind": kind,
-                "sample": f"one full cfg2a solve (refactor + IR) at N={n}; fp32 LU is "
+        return {"value": dt, "unit": "s", "cores": 1 if wl["tf"] != 2 else os.cpu_count(),
+                "kind": kind,
+                "sample": f"one full {args.config} solve (refactor + IR) at N={n}; fp32 LU is "
                           "single-threaded in the reference (mp_structures.hpp:166-167)",
                 "iters": len(rep["rhist"]) - 1, "reason": rep["reason"]}
     except Exception as e:  # pragma: no cover

@@ -207,6 +207,12 @@ int mpirg_solve_lps(int tw, int tf, int n, const void *packed, const int *ipiv, 
 int mpirg_residual(int tw, int tr, int n, const void *a, const void *x, const void *b,
                    void *r, void *stream, mpirg_error *err);
 
+/* One K5b tensor-core trailing update (lu_mode TC, binary16, nb = 64): for
+ * the panel at column k0, A22[rows k0+64..n) x [cb, ce) = fp16(fp32(A22) -
+ * L21 U12) with the 64-term product accumulated in fp32 on tcgen05.
+ * a: n x n binary16 bits, column-major, n % 8 == 0. Exposed for testing. */
+int mpirg_tc_update(int n, void *a, int k0, int cb, int ce, void *stream, mpirg_error *err);
+
 /* ---------------------------------------------------------------------------
  * Batched independent systems (BASELINE config 5b): count systems of size n,
  * each a separate MPFactorization<TW,TF,TR> + ir_solve_report with the same

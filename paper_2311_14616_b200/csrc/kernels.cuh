@@ -85,6 +85,18 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
 // perm from ipiv for callers that only hold ipiv (standalone solves).
 void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s);
 
+// K5b: tensor-core trailing update for binary16 factors (lu_tc.cu).
+struct TcPlan
+{
+  alignas(64) unsigned char mapA[128];  // CUtensorMap: L21 boxes (64 rows x 64 k)
+  alignas(64) unsigned char mapB[128];  // CUtensorMap: U12 boxes (64 k x 256 cols)
+  void *a = nullptr;
+  int n = 0;
+};
+bool tc_update_supported(int n, int nb);
+void tc_plan_make(TcPlan &p, void *a, int n);
+void launch_gemm_tc(const TcPlan &p, int k0, int cb, int ce, cudaStream_t s);
+
 // One rank of the 1-D block-cyclic LU (config 5a). a is the
 // rank's n x n factor buffer (ld n) of which it owns the column blocks
 // b with b mod G == r (block_cols columns each, a power-of-two multiple of

@@ -754,8 +754,26 @@ void panel_any(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, LuWork
     panel_tall<T, NB>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
 }
 
+// Trailing update of step k0 on columns [cb, ce): the tensor-core kernel when
+// a TC plan is given (binary16, nb = 64, full panel), else the exact SIMT one.
 template <typename T, int NB>
-void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, cudaStream_t s)
+void trailing_update(T *a, int n, int k0, int jb, int cb, int ce, const TcPlan *tc,
+                     cudaStream_t s)
+{
+  if constexpr (std::is_same<T, h16>::value && NB == 64)
+  {
+    if (tc && jb == NB)
+    {
+      launch_gemm_tc(*tc, k0, cb, ce, s);
+      return;
+    }
+  }
+  launch_gemm<T, NB>(a, n, k0, jb, cb, ce, ColMap{}, s);
+}
+
+template <typename T, int NB>
+void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, cudaStream_t s,
+            const TcPlan *tc = nullptr)
 {
   const ColMap id{};
   cudaStream_t side = static_cast<cudaStream_t>(ws.side);
@@ -786,7 +804,7 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
       if (p > 0)
         MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + p - 1], 0));
       launch_mt<T, NB>(a, n, k0, jb, c0, cnext, id, mv, nm, s);
-      launch_gemm<T, NB>(a, n, k0, jb, c0, cnext, id, s);
+      trailing_update<T, NB>(a, n, k0, jb, c0, cnext, tc, s);
     }
     MPIRG_CUDA_CHECK(cudaEventRecord(evN, s));
     // side: the rest of this step's update + the left-column moves
@@ -794,7 +812,7 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
     if (cnext < n)
     {
       launch_mt<T, NB>(a, n, k0, jb, cnext, n, id, mv, nm, side);
-      launch_gemm<T, NB>(a, n, k0, jb, cnext, n, id, side);
+      trailing_update<T, NB>(a, n, k0, jb, cnext, n, tc, side);
     }
     launch_moves<T, NB>(a, n, 0, k0, id, mv, nm, perm, side);
     MPIRG_CUDA_CHECK(cudaEventRecord(evR, side));
@@ -883,7 +901,12 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.smv, sizeof(int2) * 2 * (size_t)ws.nb));
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.snm, sizeof(int) * (size_t)ws.nb));
   cudaStream_t side;
-  MPIRG_CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  // The side stream carries the bulk trailing update; give it the lowest
+  // priority so the block scheduler hands freed SMs to the critical chain
+  // (panel -> next-panel update) on the caller's stream first.
+  int lo = 0, hi = 0;
+  MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
   ws.side = side;
   auto *ev = new cudaEvent_t[3 * (size_t)ws.npanels];
   for (int i = 0; i < 3 * ws.npanels; ++i)
@@ -911,10 +934,10 @@ void lu_workspace_free(LuWorkspace &ws)
 
 template <typename T>
 void lu_dispatch(int nb, T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
-                 cudaStream_t s)
+                 cudaStream_t s, const TcPlan *tc = nullptr)
 {
   if (nb == 64)
-    lu_run<T, 64>(a, n, ipiv, perm, ws, info, s);
+    lu_run<T, 64>(a, n, ipiv, perm, ws, info, s, tc);
   else if (nb == 32)
     lu_run<T, 32>(a, n, ipiv, perm, ws, info, s);
   else
@@ -926,7 +949,13 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
 {
   if (n <= 0)
     return;
-  (void)lu_mode;
+  if (prec == B16 && lu_mode == 1 /* MPIRG_LU_TC */ && tc_update_supported(n, ws.nb))
+  {
+    TcPlan plan;
+    tc_plan_make(plan, a, n);
+    lu_dispatch<h16>(ws.nb, static_cast<h16 *>(a), n, ipiv, perm, ws, info, s, &plan);
+    return;
+  }
   if (prec == B64)
     lu_dispatch<double>(ws.nb, static_cast<double *>(a), n, ipiv, perm, ws, info, s);
   else if (prec == B32)

@@ -215,7 +215,9 @@ struct mpirg_factorization
   void alloc()
   {
     const size_t nn = (size_t)n * n;
-    MPIRG_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;  // the handle's stream runs the LU's critical chain
+    MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
     a_high = dalloc_bytes(nn * tw_bytes());
     a_low = dalloc_bytes(nn * tf_bytes());
     ipiv = dalloc<int>(n);
@@ -1283,5 +1285,17 @@ int mpirg_dlu_end(mpirg_dlu *h, void *stream, int *singular_col, mpirg_error *er
     MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
     if (singular_col)
       *singular_col = sc == INT_MAX ? -1 : sc;
+  });
+}
+
+int mpirg_tc_update(int n, void *a, int k0, int cb, int ce, void *stream, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    if (!tc_update_supported(n, 64) || k0 < 0 || k0 + 64 > n || cb < k0 + 64 || ce > n)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "unsupported TC update geometry"};
+    require_gpu();
+    TcPlan plan;
+    tc_plan_make(plan, a, n);
+    launch_gemm_tc(plan, k0, cb, ce, static_cast<cudaStream_t>(stream));
   });
 }

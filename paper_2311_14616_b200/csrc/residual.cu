@@ -281,6 +281,8 @@ __global__ void ir_finish_kernel(int n, const TR *__restrict__ x, TW *__restrict
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() { return get_encode(); }
+
 void residual_plan_make(ResidualPlan &p, int tw, int n, const void *a)
 {
   residual_plan_free(p);
