@@ -39,7 +39,6 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "lu_panel.cuh"
-#include "lu_panel5.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -508,102 +507,6 @@ int panel_rpt(int m)
   return rpt <= max_rpt<T, NB>() ? rpt : 0;
 }
 
-template <typename T, int NB, int RPL, int IB>
-void launch_panel5(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm,
-                   DevInfo *info, cudaStream_t s)
-{
-  constexpr size_t smem = panel5::panel5_dyn_smem<T, NB, RPL, IB>();
-  static bool done = false;
-  if (!done)
-  {
-    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(panel5::lu_panel5_kernel<T, NB, RPL, IB>,
-                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(panel5::lu_panel5_kernel<T, NB, RPL, IB>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-    done = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cs);
-  cfg.blockDim = dim3(panel5::NT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel5::lu_panel5_kernel<T, NB, RPL, IB>, a, n, k0,
-                                      jb, ipiv, mv, nm, info));
-}
-
-// Block width of the critical warp's register tile for (T, rows per lane).
-template <typename T, int RPL>
-constexpr int ib_of()
-{
-  // RPL * IB * words(T) <= 128 registers
-  constexpr int words = (int)((sizeof(T) + 3) / 4);
-  return (128 / (RPL * words)) >= 8 ? 8 : ((128 / (RPL * words)) >= 4 ? 4 : 2);
-}
-
-template <typename T, int NB, int RPL>
-constexpr bool panel5_ok()
-{
-  constexpr int IB = ib_of<T, RPL>();
-  return NB % IB == 0 && (IB * sizeof(T)) % 16 == 0 &&
-         panel5::panel5_dyn_smem<T, NB, RPL, IB>() <= 200 * 1024;
-}
-
-// Experimental critical-warp panel (lu_panel5.cuh), opt-in via MPIRG_PANEL=5.
-template <typename T, int NB>
-bool launch_panel5_dispatch(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm,
-                            DevInfo *info, cudaStream_t s, int max_cs)
-{
-  const int m = n - k0;
-  int rpl = 4;
-  while (rpl * 32 * max_cs < m && rpl < 32)
-    rpl *= 2;
-  const int cs = std::max(1, (m + rpl * 32 - 1) / (rpl * 32));
-  if (cs > panel5::MAXCS)
-    return false;
-  bool launched = false;
-  if (rpl == 4)
-  {
-    if constexpr (panel5_ok<T, NB, 4>())
-    {
-      launch_panel5<T, NB, 4, ib_of<T, 4>()>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
-      launched = true;
-    }
-  }
-  else if (rpl == 8)
-  {
-    if constexpr (panel5_ok<T, NB, 8>())
-    {
-      launch_panel5<T, NB, 8, ib_of<T, 8>()>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
-      launched = true;
-    }
-  }
-  else if (rpl == 16)
-  {
-    if constexpr (panel5_ok<T, NB, 16>())
-    {
-      launch_panel5<T, NB, 16, ib_of<T, 16>()>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
-      launched = true;
-    }
-  }
-  else
-  {
-    if constexpr (panel5_ok<T, NB, 32>())
-    {
-      launch_panel5<T, NB, 32, ib_of<T, 32>()>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
-      launched = true;
-    }
-  }
-  return launched;
-}
-
 template <typename T, int NB>
 void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, DevInfo *info,
                   cudaStream_t s)
@@ -614,14 +517,8 @@ void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, Dev
   if (rpt == 0)
     throw std::runtime_error("LU panel: n too large for a single-cluster panel at this nb");
   const int cs = std::max(1, (m + rpt * per_cta - 1) / (rpt * per_cta));
-  static const bool p5 = [] {
-    const char *e = std::getenv("MPIRG_PANEL");
-    return e && std::atoi(e) == 5;
-  }();
   prof_begin(KC_PANEL, s);
-  if (p5 && launch_panel5_dispatch<T, NB>(a, n, k0, jb, ipiv, mv, nm, info, s, panel_max_cs()))
-    ;
-  else if (rpt == 1)
+  if (rpt == 1)
     launch_panel_rpt<T, NB, 1>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
   else if (rpt == 2)
   {
@@ -886,7 +783,10 @@ int lu_choose_nb(int prec, int n, int requested)
     return requested;
   if (prec == B64)
     return n <= 4096 ? 64 : (n <= 8192 ? 32 : 16);
-  return n <= 8192 ? 64 : 32;
+  // 64 at every n: panels taller than one cluster holds go through the
+  // 8-column leaves (panel_tall), and the wider step halves the trailing
+  // update's HBM passes (nb = 32 left the N = 16384 update memory-bound).
+  return 64;
 }
 
 void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)

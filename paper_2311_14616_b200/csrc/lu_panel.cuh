@@ -41,13 +41,15 @@ constexpr int NW = NT / 32;
 constexpr int MAXCS = 16;
 constexpr int IB = 8;
 
-template <typename T, int NB>
+// Per-step message of one CTA: its candidate and the candidate's current
+// block columns (the columns right of the block travel once per block).
+template <typename T>
 struct alignas(16) Slot
 {
   unsigned long long key;  // mag_key of the candidate, 0 = none
   int pos;                 // its current position (INT_MAX = none)
   int nan;                 // the row at position k holds a NaN in column k
-  T row[NB];               // the candidate row (panel columns, as of this step)
+  T blk[IB];               // the candidate's block columns, as of this step
 };
 
 // Warp-level candidate staged for the CTA reduction.
@@ -208,7 +210,9 @@ __device__ __forceinline__ uint32_t cluster_size()
 
 __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Dynamic shared memory: P[NB][R] (this CTA's rows, column-major) + Ub[IB][NB].
+// Dynamic shared memory: P[NB][R] (this CTA's rows, column-major) + Ub[IB][NB]
+// (the block's pivot rows: block columns from the step messages, right
+// columns from the block-end exchange).
 template <typename T, int NB, int RPT, int NTX = NT>
 __host__ __device__ constexpr size_t panel_dyn_smem()
 {
@@ -244,15 +248,16 @@ __global__ void __launch_bounds__(NTX, 1)
   constexpr int NT = NTX;  // hides the namespace default inside this kernel
   constexpr int NW = NTX / 32;
   static_assert(NW <= 32 && NW * 2 >= MAXCS, "push mapping needs 2*NW >= MAXCS");
-  using S = Slot<T, NB>;
+  using S = Slot<T>;
   constexpr int R = RPT * NT;
   constexpr bool WIDE = sizeof(T) > 4;
+  constexpr unsigned long long FORCED = WIDE ? ~0ull : 0xFFFFFFFFull;
   static_assert(sizeof(S) % 16 == 0, "slot must be a multiple of 16 bytes");
   static_assert(NB % IB == 0, "NB must be a multiple of IB");
   __shared__ WSlot<T> wslot[2][NW];  // double-buffered: a slow reader of step j never sees j+1
-  __shared__ S sendbuf[2];           // this CTA's candidate, assembled for the bulk push
-  __shared__ S inbox[2][MAXCS];      // every CTA's candidate (filled by bulk copies)
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ S inbox[2][MAXCS];      // every CTA's candidate (st.async from the peers)
+  __shared__ __align__(8) uint64_t bars[3];  // [0],[1]: step inboxes, [2]: block exchange
+  __shared__ int piv_rank[IB], piv_lrow[IB];  // owner CTA / local row of the block's pivots
   extern __shared__ __align__(16) unsigned char dsm[];
   T *P = reinterpret_cast<T *>(dsm);                                     // [NB][R]
   T *Ub = reinterpret_cast<T *>(dsm + a16(sizeof(T) * (size_t)NB * R));  // [IB][NB]
@@ -287,21 +292,18 @@ __global__ void __launch_bounds__(NTX, 1)
           P[(c0 + u) * R + t + q * NT] = tmp[u][q];
   }
   const bool multi = CS > 1;
-  // Bytes my inbox receives at step s: the header and the chunks from the
-  // step's block start on, from each of the CS CTAs.
-  auto step_bytes = [&](int s) -> uint32_t {
-    const int blk0 = (s / IB) * IB;
-    return (uint32_t)(CS * ((int)(sizeof(S) / 16) - (int)((blk0 * sizeof(T)) / 16)) * 16);
-  };
+  // Bytes my inbox receives per step: one message from each of the CS CTAs.
+  const uint32_t step_bytes = (uint32_t)(CS * sizeof(S));
   if (t == 0 && multi)
   {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // Arm the first two phases before any peer can send.
-    mbar_expect_tx(&bars[0], step_bytes(0));
+    mbar_expect_tx(&bars[0], step_bytes);
     if (jb > 1)
-      mbar_expect_tx(&bars[1], step_bytes(1));
+      mbar_expect_tx(&bars[1], step_bytes);
   }
   if (multi)
     cluster_sync_all();
@@ -345,6 +347,14 @@ __global__ void __launch_bounds__(NTX, 1)
     for (int q = 0; q < RPT; ++q)
       chosen[q] = IB;
     const int bend = min(jb0 + IB, jb);  // first column right of the block
+    // right-column chunks of one pivot row, from the chunk-aligned jb0 + IB on
+    const int rch = (int)(((size_t)(NB - (jb0 + IB)) * sizeof(T) + 15) / 16);
+    if (t < IB)
+      piv_rank[t] = -1;
+    // Arm the block exchange before this CTA sends any step message of the
+    // block: a peer sends block data only after every CTA's last step message.
+    if (t == 0 && multi && bend < jb)
+      mbar_expect_tx(&bars[2], (uint32_t)((bend - jb0) * rch * 16));
 
 #pragma unroll
     for (int jj = 0; jj < IB; ++jj)
@@ -355,7 +365,9 @@ __global__ void __launch_bounds__(NTX, 1)
       const int k = k0 + j;
       const int par = step & 1;
 
-      // 1. thread-local candidate among unchosen rows (positions >= k).
+      // 1. thread-local candidate among unchosen rows (positions >= k). A NaN
+      //    is never chosen, except that a NaN at position k keeps p = k
+      //    (dense_lu.hpp:65-78): that row takes the FORCED key, above any |a|.
       unsigned long long bkey = 0ull;
       int bp = INT_MAX, bq = 0, nan = 0;
 #pragma unroll
@@ -364,7 +376,15 @@ __global__ void __launch_bounds__(NTX, 1)
         if (pos[q] >= k)
         {
           if (is_nan_t(cur[q][jj]))
-            nan |= (pos[q] == k);
+          {
+            if (pos[q] == k)
+            {
+              nan = 1;
+              bkey = FORCED;
+              bp = k;
+              bq = q;
+            }
+          }
           else
           {
             const unsigned long long key = mag_key(cur[q][jj]);
@@ -417,67 +437,25 @@ __global__ void __launch_bounds__(NTX, 1)
       if (ckey == 0ull)
         cpos = INT_MAX;
       PT_MARK(3);
-      // 5. push the CTA candidate [key|pos|nan|row] to every CTA: warp w sends
-      //    to CTAs w, w+NW, ...; lane l sends 16-byte chunk l (st.async, which
-      //    completes bytes on the receiver's mbarrier). CS == 1: warp 0 just
-      //    assembles it locally.
-      const S *U;
-      int gr = 0;
+      // 5. push the CTA candidate [key|pos|nan|block columns] to every CTA:
+      //    warp w sends to CTAs w, w+NW; lane l sends 16-byte chunk l (st.async
+      //    completes bytes on the receiver's mbarrier).
+      const S *U = nullptr;
+      const T *Ublk;
+      int gr = rank;
       unsigned long long gkey = ckey;
       int gp = cpos, gn = cn;
       constexpr int NCH = sizeof(S) / 16;
-      constexpr int EPC = 16 / sizeof(T);
+      if (multi && lane < NCH)
       {
         const WSlot<T> &ws = wslot[par][cw];
-        const int lrow = ws.lrow;
-        const int ch_lo = 1 + (int)((jb0 * sizeof(T)) / 16);  // chunks left of the block: unused
-        if (multi)
-        {
-#pragma unroll
-          for (int h = 0; h < (NCH + 31) / 32; ++h)
-          {
-            const int ch = lane + 32 * h;
-            if (ch < NCH && (ch == 0 || ch >= ch_lo))
-            {
-              uint4 val;
-              if (ch == 0)
-                val = make_uint4((uint32_t)ckey, (uint32_t)(ckey >> 32), (uint32_t)cpos,
-                                 (uint32_t)cn);
-              else
-              {
-                T e[EPC];
-#pragma unroll
-                for (int w = 0; w < EPC; ++w)
-                {
-                  const int c = (ch - 1) * EPC + w;
-                  e[w] = (c < bend) ? ws.blk[c - jb0]
-                                    : ((c < jb && ckey != 0ull) ? P[c * R + lrow] : T{});
-                }
-                val = *reinterpret_cast<const uint4 *>(e);
-              }
-              for (int d = warp; d < CS; d += NW)
-                st_async_v4(push_dst[par][d >= NW] + ch * 16, val, push_bar[par][d >= NW]);
-            }
-          }
-        }
-        else if (warp == 0)
-        {
-          S &sb = sendbuf[par];
-          if (lane == 0)
-          {
-            sb.key = ckey;
-            sb.pos = cpos;
-            sb.nan = cn;
-          }
-#pragma unroll
-          for (int h = 0; h < (NB + 31) / 32; ++h)
-          {
-            const int c = jb0 + lane + 32 * h;
-            if (c < NB)
-              sb.row[c] = (c < bend) ? ws.blk[c - jb0]
-                                     : ((c < jb && ckey != 0ull) ? P[c * R + lrow] : T{});
-          }
-        }
+        uint4 val;
+        if (lane == 0)
+          val = make_uint4((uint32_t)ckey, (uint32_t)(ckey >> 32), (uint32_t)cpos, (uint32_t)cn);
+        else
+          val = reinterpret_cast<const uint4 *>(ws.blk)[lane - 1];
+        for (int d = warp; d < CS; d += NW)
+          st_async_v4(push_dst[par][d >= NW] + lane * 16, val, push_bar[par][d >= NW]);
       }
       PT_MARK(4);
       if (multi)
@@ -487,7 +465,7 @@ __global__ void __launch_bounds__(NTX, 1)
         //    this one included, has pushed step+1).
         mbar_wait(&bars[par], (uint32_t)((step >> 1) & 1));
         if (t == 0 && step + 2 < jb)
-          mbar_expect_tx(&bars[par], step_bytes(step + 2));
+          mbar_expect_tx(&bars[par], step_bytes);
         PT_MARK(5);
         // 7. global winner (identical in every thread of every CTA).
         const unsigned long long gk0 = lane < CS ? inbox[par][lane].key : 0ull;
@@ -498,13 +476,10 @@ __global__ void __launch_bounds__(NTX, 1)
              1;
         gn = __any_sync(0xffffffffu, lane < CS ? inbox[par][lane].nan : 0);
         U = &inbox[par][gr];
+        Ublk = U->blk;
       }
       else
-      {
-        __syncthreads();  // sendbuf assembled by warp 0
-        PT_MARK(5);
-        U = &sendbuf[par];
-      }
+        Ublk = wslot[par][cw].blk;  // one CTA: its winner is the pivot
       const int p = gn ? k : gp;
       if (rank == 0 && t == 0)
       {
@@ -512,16 +487,15 @@ __global__ void __launch_bounds__(NTX, 1)
         if (!gn && gkey == 1ull)  // |pivot| == +0 (key of +0.0)
           atomicMin(&info->singular_col, k);
       }
-      // keep the pivot row (stale right columns) for the block-end update
-      for (int c = bend + t; c < jb; c += NT)
-        Ub[jj * NB + c] = U->row[c];
+      (void)U;
+      // the pivot row's block columns (its right columns come at block end)
       if (t < IB)
-        Ub[jj * NB + jb0 + t] = U->row[jb0 + t];
-      const T piv = U->row[j];
+        Ub[jj * NB + jb0 + t] = Ublk[t];
+      const T piv = Ublk[jj];
       T ub[IB];
 #pragma unroll
       for (int c = jj + 1; c < IB; ++c)
-        ub[c] = U->row[jb0 + c];
+        ub[c] = Ublk[c];
       PT_MARK(6);
       // 8. positions + elimination inside the block (a NaN pivot makes U
       //    irrelevant: l = NaN).
@@ -534,6 +508,8 @@ __global__ void __launch_bounds__(NTX, 1)
           {
             pos[q] = k;  // the pivot row moves to position k
             chosen[q] = jj;
+            piv_rank[jj] = rank;
+            piv_lrow[jj] = t + q * NT;
           }
           else
           {
@@ -554,8 +530,46 @@ __global__ void __launch_bounds__(NTX, 1)
     // ---- block end: apply the block's rank-1 updates to the columns right
     // of the block, in step order.
     PT_MARK(9);
-    __syncthreads();  // Ub complete
+    __syncthreads();  // block columns of Ub, piv_rank / piv_lrow final
     const int nb_here = bend - jb0;
+    if (bend < jb)
+    {
+      // the block's pivot rows, right columns as of the block start (P is
+      // only updated at block end), from their owners to every CTA
+      const int c_lo = jb0 + IB;
+      constexpr int EPC = 16 / sizeof(T);
+      if (multi)
+      {
+        const int per_row = CS * rch;
+        for (int idx = t; idx < nb_here * per_row; idx += NT)
+        {
+          const int jj = idx / per_row, rem = idx - jj * per_row;
+          if (piv_rank[jj] != rank)
+            continue;
+          const int dst = rem / rch, ch = rem - dst * rch;
+          const int lrow = piv_lrow[jj];
+          T e[EPC];
+#pragma unroll
+          for (int w = 0; w < EPC; ++w)
+          {
+            const int c = c_lo + ch * EPC + w;
+            e[w] = c < jb ? P[c * R + lrow] : T{};
+          }
+          st_async_v4(mapa(smem_addr(Ub + jj * NB + c_lo) + ch * 16, dst),
+                      *reinterpret_cast<const uint4 *>(e), mapa(smem_addr(&bars[2]), dst));
+        }
+        mbar_wait(&bars[2], (uint32_t)((jb0 / IB) & 1));
+      }
+      else
+      {
+        for (int idx = t; idx < nb_here * (jb - bend); idx += NT)
+        {
+          const int jj = idx / (jb - bend), c = bend + idx % (jb - bend);
+          Ub[jj * NB + c] = P[c * R + piv_lrow[jj]];
+        }
+        __syncthreads();
+      }
+    }
     // (a) complete the pivot rows: U_jj[c] -= l(pivot jj, jj') * U_jj'[c], jj' < jj
     for (int c = bend + t; c < jb; c += NT)
     {

@@ -126,6 +126,34 @@ def test_lu_bitwise_any_panel_width(orc, nb, gpulib):
     np.testing.assert_array_equal(ipiv.cpu().numpy(), ipiv_want)
 
 
+@pytest.mark.parametrize("prec,n", [(B64, 200), (B32, 200), (B16, 200), (B64, 1500),
+                                    (B32, 1500)])
+@pytest.mark.parametrize("where", ["diag", "below", "inf"])
+def test_lu_nonfinite_entries(orc, prec, n, where, gpulib):
+    """dense_lu.hpp:65-78 with non-finite data: a NaN is never chosen as a
+    pivot unless it sits at position k (then p = k and the column becomes NaN);
+    Inf wins the search. Bitwise (any NaN equals any NaN) against the oracle,
+    single-CTA (n=200) and cluster (n=1500) panels."""
+    import torch
+    a64 = normal_matrix(n, 40 + n)
+    k = n // 3
+    if where == "diag":
+        a64[k, k] = np.nan
+    elif where == "below":
+        a64[k + 5, k] = np.nan
+    else:
+        a64[k + 3, k] = np.inf
+    a = demote_host(a64, prec) if prec != B64 else a64
+    st, want, ipiv_want, _, _ = orc.lu(a, prec)
+    assert st == 0
+    d = to_dev(a)
+    ipiv = torch.zeros(n, dtype=torch.int32, device="cuda")
+    K().lu_factor(d, ipiv, n)
+    got = from_dev(d, dtype=NP[prec] if prec == B16 else None)
+    np.testing.assert_array_equal(ipiv.cpu().numpy(), ipiv_want)
+    assert same_bits(got, want)
+
+
 def test_lu_singular_column(gpulib):
     """test_dense_lu.cpp:45-66: column 2 all zero -> SingularPivot(column=2)."""
     import torch
