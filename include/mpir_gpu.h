@@ -300,6 +300,15 @@ int mpirg_profile_collect(double *ms, int *count, int nclass);
 /* Runs a pure-FFMA kernel on the current device; *tflops = achieved fp32 FMA
  * rate (2 flops per FFMA), *ms = its duration. */
 int mpirg_ffma_peak(double *tflops, double *ms);
+/* The same for binary64 DFMA (the roofline denominator of the fp64 chains:
+ * residual and one-norm at small n, where rows/columns < lanes x SMSPs). */
+int mpirg_dfma_peak(double *tflops, double *ms);
+/* Diagnostics: compares the reciprocal-based division used on the back
+ * substitution's critical path (common.cuh div_rcp) with IEEE div.rn on
+ * `count` seeded operand pairs of precision `prec` (MPIRG_B64 / MPIRG_B32);
+ * *mismatches = differing results, example[0..1] = one offending (a, b). */
+int mpirg_check_fast_div(int prec, unsigned long long seed, long long count,
+                         long long *mismatches, double *example);
 
 /* ---------------------------------------------------------------------------
  * Seeded input generators (host; not on the timed path). See problems.cpp.

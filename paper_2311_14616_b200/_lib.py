@@ -12,7 +12,9 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmpir_gpu.so")
+# MPIRG_LIB selects an in-tree build variant (e.g. the instrumented panel build
+# of tools/); default: the product library.
+LIB_PATH = os.path.join(HERE, os.environ.get("MPIRG_LIB", "libmpir_gpu.so"))
 HEADER = os.path.join(os.path.dirname(HERE), "include", "mpir_gpu.h")
 
 B64, B32, B16 = 0, 1, 2
@@ -156,6 +158,9 @@ PROTOTYPES = {
     "mpirg_profile_enable": (None, [_I]),
     "mpirg_profile_collect": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_int), _I]),
     "mpirg_ffma_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "mpirg_dfma_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "mpirg_check_fast_div": (_I, [C.c_int, C.c_ulonglong, C.c_longlong,
+                                  C.POINTER(C.c_longlong), C.POINTER(C.c_double)]),
     "mpirg_gen_uniform_matrix": (None, [_I, _I, C.c_uint64, _D, _D, _P]),
     "mpirg_gen_normal_matrix": (None, [_I, _I, C.c_uint64, _P]),
     "mpirg_gen_diag_dominant": (None, [_I, C.c_uint64, _D, _P]),

@@ -99,24 +99,33 @@ __device__ __forceinline__ double acc_add(double s, double v) { return __dadd_rn
 __device__ __forceinline__ float acc_add(float s, float v) { return __fadd_rn(s, v); }
 __device__ __forceinline__ h16 acc_add(h16 s, h16 v) { return hadd(s, v); }
 
-// Fused cast + one-norm. One warp owns a stripe of 32 columns and walks down
-// the rows in 32x32 tiles: lane = row for the coalesced load/demote/store,
-// then lane = column for the in-order column sum through a padded smem tile.
+// Fused cast + one-norm. A CTA owns a stripe of CN = 16 columns and walks
+// down the rows in chunks of 256. Eight loader warps (lane = row) do the
+// coalesced load / demote / store of the chunk -- every element independent --
+// and deposit |x| into a double-buffered, padded smem tile; a ninth warp
+// (lane = column) performs the reference's strictly sequential per-column sum
+// over the previous chunk while the loaders already stream the next one. The
+// sum chain (n dependent adds per column) is therefore the only serial part,
+// and it overlaps the HBM stream instead of gating it.
 // To == From (TF == TW) is a plain copy. NORM_ONLY skips the store.
+constexpr int CN = 16;            // columns per CTA
+constexpr int CLW = 8;            // loader warps
+constexpr int CCH = CLW * 32;     // rows per chunk
+constexpr int CAST_NT = CLW * 32 + 32;
+
 template <typename From, typename To, bool NORM_ONLY>
-__global__ void __launch_bounds__(128) cast_norm_kernel(const From *__restrict__ src,
-                                                        To *__restrict__ dst, int rows,
-                                                        int cols,
-                                                        unsigned long long *norm_bits,
-                                                        DevInfo *info)
+__global__ void __launch_bounds__(CAST_NT) cast_norm_kernel(const From *__restrict__ src,
+                                                            To *__restrict__ dst, int rows,
+                                                            int cols,
+                                                            unsigned long long *norm_bits,
+                                                            DevInfo *info)
 {
-  __shared__ From tile[4][32][33];
+  extern __shared__ __align__(16) unsigned char cast_sm[];
+  auto tile = reinterpret_cast<From(*)[CN][CCH + 1]>(cast_sm);  // [2][CN][CCH+1]
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int c0 = (blockIdx.x * 4 + w) * 32;
-  if (c0 >= cols)
-    return;
-  const int ncol = min(32, cols - c0);
+  const int c0 = blockIdx.x * CN;
+  const int ncol = min(CN, cols - c0);
   const double maxf =
       NORM_ONLY ? 0.0
                 : max_finite_of(std::is_same<To, double>::value
@@ -124,62 +133,77 @@ __global__ void __launch_bounds__(128) cast_norm_kernel(const From *__restrict__
                                     : (std::is_same<To, float>::value ? B32 : B16));
   bool uf = false;
   unsigned long long ovf = ~0ull;
-  From sum = From{};
+  From sum;
   if constexpr (std::is_same<From, h16>::value)
     sum = h16{0};
   else
     sum = From(0);
+  const int nchunks = (rows + CCH - 1) / CCH;
 
-  From cur[32], nxt[32];
-  auto load_tile = [&](int r0, From *v) {
-    const int r = r0 + lane;
+  From cur[CN];
+  auto load = [&](int ch) {
+    const int r = ch * CCH + w * 32 + lane;
 #pragma unroll
-    for (int c = 0; c < 32; ++c)
-    {
-      if (c < ncol && r < rows)
-        v[c] = ldcs_t(src + (size_t)(c0 + c) * rows + r);
-      else
-        v[c] = From{};
-    }
+    for (int c = 0; c < CN; ++c)
+      cur[c] = (c < ncol && r < rows) ? ldcs_t(src + (size_t)(c0 + c) * rows + r) : From{};
   };
-  load_tile(0, cur);
-  for (int r0 = 0; r0 < rows; r0 += 32)
+  if (w < CLW && nchunks > 0)
+    load(0);
+  for (int ch = 0; ch <= nchunks; ++ch)
   {
-    if (r0 + 32 < rows)
-      load_tile(r0 + 32, nxt);
-    const int r = r0 + lane;
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
+    if (w < CLW)
     {
-      if (c < ncol && r < rows)
+      if (ch < nchunks)
       {
-        if constexpr (!NORM_ONLY)
+        const int rr = w * 32 + lane;
+        const int r = ch * CCH + rr;
+        From (*tb)[CCH + 1] = tile[ch & 1];
+#pragma unroll
+        for (int c = 0; c < CN; ++c)
         {
-          const size_t idx = (size_t)(c0 + c) * rows + r;
-          dst[idx] = demote_one<From, To>(cur[c], idx, maxf, uf, ovf);
+          if (c < ncol && r < rows)
+          {
+            if constexpr (!NORM_ONLY)
+            {
+              const size_t idx = (size_t)(c0 + c) * rows + r;
+              dst[idx] = demote_one<From, To>(cur[c], idx, maxf, uf, ovf);
+            }
+          }
+          tb[c][rr] = absv(cur[c]);
         }
-        tile[w][c][lane] = absv(cur[c]);
+        if (ch + 1 < nchunks)
+          load(ch + 1);
       }
     }
-    __syncwarp();
-    const int nr = min(32, rows - r0);
-    if (lane < ncol)
+    else if (ch > 0 && lane < ncol)
     {
-      for (int i = 0; i < nr; ++i)
-        sum = acc_add(sum, tile[w][lane][i]);
+      // the sequential column sum over chunk ch-1, rows in order
+      const From *tr = tile[(ch - 1) & 1][lane];
+      const int nr = min(CCH, rows - (ch - 1) * CCH);
+      if (nr == CCH)
+      {
+#pragma unroll 16
+        for (int i = 0; i < CCH; ++i)
+          sum = acc_add(sum, tr[i]);
+      }
+      else
+      {
+        for (int i = 0; i < nr; ++i)
+          sum = acc_add(sum, tr[i]);
+      }
     }
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-      cur[c] = nxt[c];
+    __syncthreads();
   }
-  // best = std::max(best, double(s)): NaN sums never win; sums are >= 0.
-  const double sd = lane < ncol ? to_d(sum) : 0.0;
-  unsigned long long bits = isnan(sd) ? 0ull : abs_bits(sd);
-  bits = warp_max_u64(bits);
-  if (lane == 0)
-    atomicMax(norm_bits, bits);
-  if constexpr (!NORM_ONLY)
+  if (w == CLW)
+  {
+    // best = std::max(best, double(s)): NaN sums never win; sums are >= 0.
+    const double sd = lane < ncol ? to_d(sum) : 0.0;
+    unsigned long long bits = isnan(sd) ? 0ull : abs_bits(sd);
+    bits = warp_max_u64(bits);
+    if (lane == 0)
+      atomicMax(norm_bits, bits);
+  }
+  else if constexpr (!NORM_ONLY)
     flush_flags(uf, ovf, info);
 }
 
@@ -204,10 +228,17 @@ void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long l
 {
   if (rows <= 0 || cols <= 0)
     return;
-  const int stripes = (cols + 31) / 32;
-  const int grid = (stripes + 3) / 4;
+  const int grid = (cols + CN - 1) / CN;
+  constexpr int smem = (int)(sizeof(From) * 2 * CN * (CCH + 1));
+  static bool configured = false;
+  if (!configured)
+  {
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(cast_norm_kernel<From, To, NORM_ONLY>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
   ProfScope ps(KC_CAST, s);
-  cast_norm_kernel<From, To, NORM_ONLY><<<grid, 128, 0, s>>>(
+  cast_norm_kernel<From, To, NORM_ONLY><<<grid, CAST_NT, smem, s>>>(
       static_cast<const From *>(src), static_cast<To *>(dst), rows, cols, nb, info);
   MPIRG_CUDA_CHECK(cudaGetLastError());
 }

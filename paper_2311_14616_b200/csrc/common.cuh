@@ -91,6 +91,62 @@ __device__ __forceinline__ double divide(double a, double b) { return __ddiv_rn(
 __device__ __forceinline__ float divide(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ h16 divide(h16 a, h16 b) { return hdiv(a, b); }
 
+// ---------------------------------------------------------------------------
+// IEEE division from a precomputed reciprocal, for divisions on a sequential
+// critical path whose divisor is known early (the diagonal of U in the back
+// substitution). With y = RN(1/b):
+//   q0 = RN(a*y)                   (within 1.5 ulp of a/b)
+//   q1 = q0 + RN(a - b*q0) * y     (within 1 ulp)
+//   q2 = q1 + RN(a - b*q1) * y     (Markstein: q2 = RN(a/b))
+// i.e. one multiply and four dependent FMAs instead of MUFU.RCP + the Newton
+// sequence + FCHK of div.rn. Valid while a, b and a/b stay away from the
+// subnormal and overflow ranges and a != 0 (signed zeros): the caller
+// passes ok = rcp_ok(b) computed with y, and div_rcp also checks a; anything
+// else takes the IEEE division. Checked bitwise against div.rn by
+// mpirg_check_fast_div (tests/test_gpu_kernels.py).
+struct RcpF
+{
+  float y;
+  bool ok;
+};
+struct RcpD
+{
+  double y;
+  bool ok;
+};
+__device__ __forceinline__ bool exp_mid_f(float v)
+{
+  const unsigned e = (__float_as_uint(v) >> 23) & 0xffu;
+  return e - 67u <= 120u;  // |v| in [2^-60, 2^61)
+}
+__device__ __forceinline__ bool exp_mid_d(double v)
+{
+  const unsigned e = (unsigned)((unsigned long long)__double_as_longlong(v) >> 52) & 0x7ffu;
+  return e - 523u <= 1000u;  // |v| in [2^-500, 2^501)
+}
+__device__ __forceinline__ RcpF make_rcp(float b) { return RcpF{__frcp_rn(b), exp_mid_f(b)}; }
+__device__ __forceinline__ RcpD make_rcp(double b) { return RcpD{__drcp_rn(b), exp_mid_d(b)}; }
+__device__ __forceinline__ float div_rcp(float a, float b, RcpF r)
+{
+  if (r.ok && exp_mid_f(a))
+  {
+    const float q0 = __fmul_rn(a, r.y);
+    const float q1 = __fmaf_rn(__fmaf_rn(-b, q0, a), r.y, q0);
+    return __fmaf_rn(__fmaf_rn(-b, q1, a), r.y, q1);
+  }
+  return __fdiv_rn(a, b);
+}
+__device__ __forceinline__ double div_rcp(double a, double b, RcpD r)
+{
+  if (r.ok && exp_mid_d(a))
+  {
+    const double q0 = __dmul_rn(a, r.y);
+    const double q1 = __fma_rn(__fma_rn(-b, q0, a), r.y, q0);
+    return __fma_rn(__fma_rn(-b, q1, a), r.y, q1);
+  }
+  return __ddiv_rn(a, b);
+}
+
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }

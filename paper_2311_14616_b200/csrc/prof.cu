@@ -6,10 +6,12 @@
 // default) it costs one branch per launch.
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <mutex>
 #include <vector>
 
 #include "../../include/mpir_gpu.h"
+#include "common.cuh"
 #include "kernels.cuh"
 
 namespace mpirg
@@ -113,53 +115,56 @@ int mpirg_profile_collect(double *ms, int *count, int nclass)
 
 }  // extern "C"
 
-// ---- FP32 FFMA peak microbenchmark -------------------------------------------
+// ---- FP32 FFMA / FP64 DFMA peak microbenchmarks ------------------------------
 namespace
 {
-template <bool IMM>
-__global__ void __launch_bounds__(256) ffma_peak_kernel(float *out, int iters, float b, float c)
+__device__ __forceinline__ float fma_t(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_t(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <typename T, bool IMM>
+__global__ void __launch_bounds__(256) fma_peak_kernel(T *out, int iters, T b, T c)
 {
-  float a[8];
+  T a[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    a[j] = (float)(threadIdx.x + j) * 1e-3f;
+    a[j] = (T)(threadIdx.x + j) * (T)1e-3;
   for (int i = 0; i < iters; ++i)
   {
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      a[j] = IMM ? __fmaf_rn(a[j], 1.0001f, 0.9999f) : __fmaf_rn(a[j], b, c);
+      a[j] = IMM ? fma_t(a[j], (T)1.0001, (T)0.9999) : fma_t(a[j], b, c);
   }
-  float s = 0.0f;
+  T s = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     s += a[j];
-  if (s == 12345.678f)
+  if (s == (T)12345.678)
     out[blockIdx.x] = s;
 }
-}  // namespace
 
-extern "C" int mpirg_ffma_peak(double *tflops, double *ms_out)
+template <typename T>
+int fma_peak(double *tflops, double *ms_out, int iters)
 {
   try
   {
     int dev = 0, sms = 0;
     MPIRG_CUDA_CHECK(cudaGetDevice(&dev));
     MPIRG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    float *out = nullptr;
-    MPIRG_CUDA_CHECK(cudaMalloc(&out, sizeof(float) * sms * 8));
+    T *out = nullptr;
+    MPIRG_CUDA_CHECK(cudaMalloc(&out, sizeof(T) * sms * 8));
     cudaEvent_t e0, e1;
     MPIRG_CUDA_CHECK(cudaEventCreate(&e0));
     MPIRG_CUDA_CHECK(cudaEventCreate(&e1));
-    const int blocks = sms * 8, threads = 256, iters = 8192;
+    const int blocks = sms * 8, threads = 256;
     double best = 0.0, best_ms = 0.0;
     for (int variant = 0; variant < 2; ++variant)
       for (int rep = 0; rep < 4; ++rep)
       {
         MPIRG_CUDA_CHECK(cudaEventRecord(e0));
         if (variant == 0)
-          ffma_peak_kernel<false><<<blocks, threads>>>(out, iters, 1.0001f, 0.9999f);
+          fma_peak_kernel<T, false><<<blocks, threads>>>(out, iters, (T)1.0001, (T)0.9999);
         else
-          ffma_peak_kernel<true><<<blocks, threads>>>(out, iters, 1.0001f, 0.9999f);
+          fma_peak_kernel<T, true><<<blocks, threads>>>(out, iters, (T)1.0001, (T)0.9999);
         MPIRG_CUDA_CHECK(cudaEventRecord(e1));
         MPIRG_CUDA_CHECK(cudaEventSynchronize(e1));
         float ms = 0.0f;
@@ -177,6 +182,131 @@ extern "C" int mpirg_ffma_peak(double *tflops, double *ms_out)
     cudaFree(out);
     *tflops = best;
     *ms_out = best_ms;
+    return MPIRG_OK;
+  }
+  catch (const std::exception &)
+  {
+    return MPIRG_ERR_CUDA;
+  }
+}
+}  // namespace
+
+extern "C" int mpirg_ffma_peak(double *tflops, double *ms_out)
+{
+  return fma_peak<float>(tflops, ms_out, 8192);
+}
+
+extern "C" int mpirg_dfma_peak(double *tflops, double *ms_out)
+{
+  return fma_peak<double>(tflops, ms_out, 1024);
+}
+
+// ---- self-check of div_rcp (common.cuh) against the IEEE division ------------
+namespace
+{
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z)
+{
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// Operand classes: 0 random bit patterns (every exponent, specials), 1 random
+// mid-range a / b, 2 b with a near-all-ones or near-power-of-two significand.
+template <typename T>
+__device__ T draw(unsigned long long h, int cls, bool divisor)
+{
+  if constexpr (sizeof(T) == 4)
+  {
+    unsigned bits = (unsigned)h;
+    if (cls >= 1)
+      bits = (bits & 0x807fffffu) | ((unsigned)(127 - 70 + (h >> 40) % 141) << 23);
+    if (cls == 2 && divisor)
+    {
+      const unsigned low = (unsigned)(h >> 48) & 0xfffu;
+      bits = (bits & 0xff800000u) | ((h >> 33) & 1 ? (0x7fffffu - low) : low);
+    }
+    return __uint_as_float(bits);
+  }
+  else
+  {
+    unsigned long long bits = h;
+    if (cls >= 1)
+      bits = (bits & 0x800fffffffffffffull) |
+             ((unsigned long long)(1023 - 520 + (mix64(h) % 1041)) << 52);
+    if (cls == 2 && divisor)
+    {
+      const unsigned long long low = mix64(h ^ 0x5555ull) & 0xffffull;
+      bits = (bits & 0xfff0000000000000ull) |
+             ((mix64(h) & 1) ? (0xfffffffffffffull - low) : low);
+    }
+    return __longlong_as_double((long long)bits);
+  }
+}
+
+template <typename T>
+__global__ void check_div_kernel(unsigned long long seed, long long count,
+                                 unsigned long long *bad, T *ex)
+{
+  unsigned long long nbad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+  {
+    const unsigned long long h1 = mix64(seed * 0x100000001b3ull + 2 * i);
+    const unsigned long long h2 = mix64(seed * 0x100000001b3ull + 2 * i + 1);
+    const int cls = (int)(i % 3);
+    const T a = draw<T>(h1, cls, false), b = draw<T>(h2, cls, true);
+    const T want = mpirg::divide(a, b);
+    const T got = mpirg::div_rcp(a, b, mpirg::make_rcp(b));
+    const bool same = (want == got && signbit(want) == signbit(got)) || (isnan(want) && isnan(got));
+    if (!same)
+    {
+      ++nbad;
+      ex[0] = a;
+      ex[1] = b;
+    }
+  }
+  if (nbad)
+    atomicAdd(bad, nbad);
+}
+}  // namespace
+
+extern "C" int mpirg_check_fast_div(int prec, unsigned long long seed, long long count,
+                                    long long *mismatches, double *example)
+{
+  try
+  {
+    unsigned long long *bad = nullptr;
+    double *ex = nullptr;
+    MPIRG_CUDA_CHECK(cudaMalloc(&bad, sizeof(unsigned long long)));
+    MPIRG_CUDA_CHECK(cudaMalloc(&ex, 2 * sizeof(double)));
+    MPIRG_CUDA_CHECK(cudaMemset(bad, 0, sizeof(unsigned long long)));
+    MPIRG_CUDA_CHECK(cudaMemset(ex, 0, 2 * sizeof(double)));
+    if (prec == mpirg::B64)
+      check_div_kernel<double><<<148 * 8, 256>>>(seed, count, bad, ex);
+    else
+      check_div_kernel<float><<<148 * 8, 256>>>(seed, count, bad, reinterpret_cast<float *>(ex));
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+    unsigned long long h = 0;
+    double hex[2] = {0, 0};
+    MPIRG_CUDA_CHECK(cudaMemcpy(&h, bad, sizeof(h), cudaMemcpyDeviceToHost));
+    MPIRG_CUDA_CHECK(cudaMemcpy(hex, ex, sizeof(hex), cudaMemcpyDeviceToHost));
+    if (prec != mpirg::B64)
+    {
+      float f[2];
+      std::memcpy(f, hex, sizeof(f));
+      hex[0] = f[0];
+      hex[1] = f[1];
+    }
+    cudaFree(bad);
+    cudaFree(ex);
+    *mismatches = (long long)h;
+    if (example)
+    {
+      example[0] = hex[0];
+      example[1] = hex[1];
+    }
     return MPIRG_OK;
   }
   catch (const std::exception &)

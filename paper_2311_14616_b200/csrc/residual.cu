@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -91,22 +92,52 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
       : "memory");
 }
 
-template <typename TW, typename TR, int STAGES>
+__device__ __forceinline__ void bulk_load_1d(void *dst, const void *src, uint32_t bytes,
+                                             uint64_t *bar)
+{
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename TW, typename TR, int STAGES, int RPW>
 __global__ void __launch_bounds__(32) residual_tma_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           int n, const TR *__restrict__ x,
                                                           const TW *__restrict__ b,
                                                           TR *__restrict__ r,
                                                           unsigned long long *rnorm_bits)
 {
+  // RPW rows per warp (lanes >= RPW idle): at small n there are fewer rows
+  // than lanes x SMSPs, so narrower warps spread the n independent chains
+  // over more SM sub-partitions.
+  // Each stage holds the RPW x RES_BC tile of A and the matching RES_BC-slice
+  // of x (one bulk copy on the same mbarrier), so the per-column x values
+  // come from shared memory instead of a global load per group of columns.
   extern __shared__ __align__(128) unsigned char sm[];
-  TW *tiles = reinterpret_cast<TW *>(sm);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + (size_t)STAGES * RES_BC * 32 * sizeof(TW));
+  constexpr int TILE_E = RES_BC * RPW;
+  constexpr uint32_t kBytes = TILE_E * sizeof(TW);
+  constexpr uint32_t xBytes = RES_BC * sizeof(TR);
+  constexpr size_t STAGE_B = kBytes + xBytes;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + (size_t)STAGES * STAGE_B);
   const int lane = threadIdx.x;
-  const int r0 = blockIdx.x * 32;
+  const int r0 = blockIdx.x * RPW;
   const int row = r0 + lane;
-  const bool valid = row < n;
+  const bool valid = lane < RPW && row < n;
   const int ntiles = (n + RES_BC - 1) / RES_BC;
-  constexpr uint32_t kBytes = RES_BC * 32 * sizeof(TW);
+  const int nfull = n / RES_BC;  // tiles whose x slice is a whole bulk copy
+  auto stage_tile = [&](int st) { return reinterpret_cast<TW *>(sm + (size_t)st * STAGE_B); };
+  auto stage_x = [&](int st) {
+    return reinterpret_cast<TR *>(sm + (size_t)st * STAGE_B + kBytes);
+  };
+  auto issue = [&](int st, int t) {
+    const bool fullx = t < nfull;
+    mbar_expect_tx(bars + st, kBytes + (fullx ? xBytes : 0u));
+    tma_load_2d(stage_tile(st), &tmap, bars + st, r0, t * RES_BC);
+    if (fullx)
+      bulk_load_1d(stage_x(st), x + (size_t)t * RES_BC, xBytes, bars + st);
+  };
 
   if (lane == 0)
   {
@@ -115,38 +146,37 @@ __global__ void __launch_bounds__(32) residual_tma_kernel(const __grid_constant_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
     for (int s = 0; s < STAGES && s < ntiles; ++s)
-    {
-      mbar_expect_tx(bars + s, kBytes);
-      tma_load_2d(tiles + (size_t)s * RES_BC * 32, &tmap, bars + s, r0, s * RES_BC);
-    }
+      issue(s, s);
   }
   __syncwarp();
 
+  const int lr = lane < RPW ? lane : 0;
   TR s = valid ? prom<TR, TW>(b[row]) : TR(0);
   TR c = TR(0);
   for (int t = 0; t < ntiles; ++t)
   {
     const int st = t % STAGES;
     mbar_wait(bars + st, (uint32_t)((t / STAGES) & 1));
-    const TW *tile = tiles + (size_t)st * RES_BC * 32;
+    const TW *tile = stage_tile(st);
     const int j0 = t * RES_BC;
-    if (j0 + RES_BC <= n)
+    if (lane < RPW)
     {
+      if (t < nfull)
+      {
+        const TR *xs = stage_x(st);
 #pragma unroll 16
-      for (int jj = 0; jj < RES_BC; ++jj)
-        two_sum_step<TR>(prom<TR, TW>(tile[jj * 32 + lane]), __ldg(x + j0 + jj), s, c);
-    }
-    else
-    {
-      for (int jj = 0; jj < n - j0; ++jj)
-        two_sum_step<TR>(prom<TR, TW>(tile[jj * 32 + lane]), __ldg(x + j0 + jj), s, c);
+        for (int jj = 0; jj < RES_BC; ++jj)
+          two_sum_step<TR>(prom<TR, TW>(tile[jj * RPW + lr]), xs[jj], s, c);
+      }
+      else
+      {
+        for (int jj = 0; jj < n - j0; ++jj)
+          two_sum_step<TR>(prom<TR, TW>(tile[jj * RPW + lr]), __ldg(x + j0 + jj), s, c);
+      }
     }
     __syncwarp();
     if (lane == 0 && t + STAGES < ntiles)
-    {
-      mbar_expect_tx(bars + st, kBytes);
-      tma_load_2d(tiles + (size_t)st * RES_BC * 32, &tmap, bars + st, r0, (t + STAGES) * RES_BC);
-    }
+      issue(st, t + STAGES);
   }
   TR rv = add(s, c);
   unsigned long long bits = 0;
@@ -214,10 +244,48 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
   return fn;
 }
 
-template <int STAGES>
+template <int STAGES, int RPW>
 int res_stages_smem(int esz)
 {
-  return STAGES * RES_BC * 32 * esz + STAGES * 8;
+  return STAGES * (RES_BC * RPW * esz + RES_BC * 8) + STAGES * 8;
+}
+
+// Rows per warp for the TMA path: the widest warp that still gives every SM
+// sub-partition (148 x 4) at least one row chain. MPIRG_RES_RPW overrides.
+int residual_rpw(int n)
+{
+  static const int forced = [] {
+    const char *e = std::getenv("MPIRG_RES_RPW");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 8 || forced == 16 || forced == 32)
+    return forced;
+  if (n / 32 >= 148 * 4)
+    return 32;
+  if (n / 16 >= 148 * 4)
+    return 16;
+  return 8;
+}
+
+template <typename TW, typename TR, int RPW>
+void residual_tma_launch(const ResidualPlan &p, const void *x, const void *b, void *r,
+                         unsigned long long *rb, cudaStream_t s)
+{
+  constexpr int ST = 4;
+  const int n = p.n;
+  const int smem = res_stages_smem<ST, RPW>(sizeof(TW));
+  static bool configured = false;
+  if (!configured)
+  {
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(residual_tma_kernel<TW, TR, ST, RPW>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  CUtensorMap map;
+  std::memcpy(&map, static_cast<const CUtensorMap *>(p.tmap) + (RPW == 32 ? 0 : RPW == 16 ? 1 : 2),
+              sizeof(CUtensorMap));
+  residual_tma_kernel<TW, TR, ST, RPW><<<(n + RPW - 1) / RPW, 32, smem, s>>>(
+      map, n, static_cast<const TR *>(x), static_cast<const TW *>(b), static_cast<TR *>(r), rb);
 }
 
 template <typename TW, typename TR>
@@ -227,21 +295,16 @@ void residual_t(const ResidualPlan &p, const void *x, const void *b, void *r,
   const int n = p.n;
   const int grid = (n + 31) / 32;
   ProfScope ps(KC_RESID, s);
-  if (p.tmap)
+  // the TMA path bulk-copies x slices: x must be 16-byte aligned too
+  if (p.tmap && reinterpret_cast<uintptr_t>(x) % 16 == 0)
   {
-    constexpr int ST = 4;
-    const int smem = res_stages_smem<ST>(sizeof(TW));
-    static bool configured = false;
-    if (!configured)
-    {
-      MPIRG_CUDA_CHECK(cudaFuncSetAttribute(residual_tma_kernel<TW, TR, ST>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      configured = true;
-    }
-    CUtensorMap map;
-    std::memcpy(&map, p.tmap, sizeof(CUtensorMap));
-    residual_tma_kernel<TW, TR, ST><<<grid, 32, smem, s>>>(
-        map, n, static_cast<const TR *>(x), static_cast<const TW *>(b), static_cast<TR *>(r), rb);
+    const int rpw = residual_rpw(n);
+    if (rpw == 32)
+      residual_tma_launch<TW, TR, 32>(p, x, b, r, rb, s);
+    else if (rpw == 16)
+      residual_tma_launch<TW, TR, 16>(p, x, b, r, rb, s);
+    else
+      residual_tma_launch<TW, TR, 8>(p, x, b, r, rb, s);
   }
   else
   {
@@ -293,27 +356,31 @@ void residual_plan_make(ResidualPlan &p, int tw, int n, const void *a)
   const bool aligned = ((size_t)n * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(a) % 16) == 0;
   if (!aligned || n < 32)
     return;
-  CUtensorMap *map = new CUtensorMap;
+  // one map per rows-per-warp box height (32, 16, 8)
+  CUtensorMap *map = new CUtensorMap[3];
   cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
   cuuint64_t strides[1] = {(cuuint64_t)n * esz};
-  cuuint32_t box[2] = {32, (cuuint32_t)RES_BC};
   cuuint32_t estr[2] = {1, 1};
-  const CUresult rc = get_encode()(
-      map, tw == B64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-      const_cast<void *>(a), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (rc != CUDA_SUCCESS)
+  for (int v = 0; v < 3; ++v)
   {
-    delete map;
-    return;  // fall back to the plain-load path
+    cuuint32_t box[2] = {(cuuint32_t)(32 >> v), (cuuint32_t)RES_BC};
+    const CUresult rc = get_encode()(
+        map + v, tw == B64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+        const_cast<void *>(a), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS)
+    {
+      delete[] map;
+      return;  // fall back to the plain-load path
+    }
   }
   p.tmap = map;
 }
 
 void residual_plan_free(ResidualPlan &p)
 {
-  delete static_cast<CUtensorMap *>(p.tmap);
+  delete[] static_cast<CUtensorMap *>(p.tmap);
   p = ResidualPlan{};
 }
 

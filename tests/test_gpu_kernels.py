@@ -247,3 +247,18 @@ def test_residual_bitwise(orc, tw, tr, n, gpulib):
     r = torch.zeros(n, dtype=torch.float64 if tr == B64 else torch.float32, device="cuda")
     K().residual(to_dev(a), to_dev(x), to_dev(b), r)
     assert same_bits(r.cpu().numpy(), want)
+
+
+# ------------------------------------------- reciprocal-based division --
+@pytest.mark.parametrize("prec", [B64, B32])
+def test_fast_division_matches_div_rn(prec, gpulib):
+    """The back substitution divides by u_kk through a precomputed RN(1/u_kk)
+    and two residual corrections (common.cuh div_rcp); it must equal the
+    IEEE division bit for bit, specials and range fallbacks included."""
+    import ctypes as C
+    bad = C.c_longlong(-1)
+    ex = (C.c_double * 2)()
+    for seed in (1, 2, 3):
+        rc = gpulib.mpirg_check_fast_div(prec, seed, 1 << 26, C.byref(bad), ex)
+        assert rc == 0
+        assert bad.value == 0, (prec, seed, bad.value, ex[0], ex[1])
