@@ -123,6 +123,8 @@ struct TrsvWorkspace
   int nblk = 0;
   int *flags = nullptr;    // [2][nblk] ready flags (lower, upper), epoch-tagged
   int *tickets = nullptr;  // [2] block tickets
+  unsigned long long *xw = nullptr;  // [2][n] tagged hand-off words (binary32/16 x)
+  int cap_blk = 0, cap_n = 0;        // allocated capacities
   int epoch = 0;
 };
 void trsv_workspace_alloc(TrsvWorkspace &ws, int n);

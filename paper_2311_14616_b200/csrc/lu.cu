@@ -457,6 +457,17 @@ void configure_gemm()
   done = true;
 }
 
+// Speculative pivoting in the panel (lu_panel.cuh); MPIRG_PANEL_SPEC=0 turns
+// it off (every step then takes the cluster-wide exchange).
+static int panel_spec()
+{
+  static const int v = [] {
+    const char *e = std::getenv("MPIRG_PANEL_SPEC");
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : 1;
+  }();
+  return v;
+}
+
 template <typename T, int NB, int RPT, int NTX = panel2::NT>
 void launch_panel_rpt(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm,
                       DevInfo *info, cudaStream_t s)
@@ -475,7 +486,7 @@ void launch_panel_rpt(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT, NTX>, a, n, k0,
-                                      jb, ipiv, mv, nm, info));
+                                      jb, ipiv, mv, nm, info, panel_spec()));
 }
 
 // Largest rows-per-thread the shared memory allows for (T, NB) at 256 threads.

@@ -243,7 +243,8 @@ __host__ __device__ constexpr size_t panel_dyn_smem()
 template <typename T, int NB, int RPT, int NTX = NT>
 __global__ void __launch_bounds__(NTX, 1)
     lu_panel2_kernel(T *__restrict__ A, int n, int k0, int jb, int *__restrict__ ipiv,
-                     int2 *__restrict__ moves, int *__restrict__ nmoves, DevInfo *info)
+                     int2 *__restrict__ moves, int *__restrict__ nmoves, DevInfo *info,
+                     int spec_ok)
 {
   constexpr int NT = NTX;  // hides the namespace default inside this kernel
   constexpr int NW = NTX / 32;
@@ -256,7 +257,13 @@ __global__ void __launch_bounds__(NTX, 1)
   static_assert(NB % IB == 0, "NB must be a multiple of IB");
   __shared__ WSlot<T> wslot[2][NW];  // double-buffered: a slow reader of step j never sees j+1
   __shared__ S inbox[2][MAXCS];      // every CTA's candidate (st.async from the peers)
-  __shared__ __align__(8) uint64_t bars[3];  // [0],[1]: step inboxes, [2]: block exchange
+  // [0],[1]: exchange-step inboxes, [2]: block exchange, [3],[4]: block
+  // verification flags, [5 + jj]: speculative step jj of a block
+  __shared__ __align__(8) uint64_t bars[5 + IB];
+  __shared__ S sinbox[IB];                 // speculative pivot rows (one sender per step)
+  __shared__ S sstage[NW];                 // the sending warp's staged message
+  __shared__ uint32_t vflag[2][MAXCS];     // every CTA's "speculation beaten" flag
+  __shared__ int cta_beaten;
   __shared__ int piv_rank[IB], piv_lrow[IB];  // owner CTA / local row of the block's pivots
   extern __shared__ __align__(16) unsigned char dsm[];
   T *P = reinterpret_cast<T *>(dsm);                                     // [NB][R]
@@ -296,15 +303,22 @@ __global__ void __launch_bounds__(NTX, 1)
   const uint32_t step_bytes = (uint32_t)(CS * sizeof(S));
   if (t == 0 && multi)
   {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], 1);
+    for (int i = 0; i < 5 + IB; ++i)
+      mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // Arm the first two phases before any peer can send.
+    // Arm every first phase before any peer can send: the exchange steps'
+    // two parities, both verification parities, each speculative step.
     mbar_expect_tx(&bars[0], step_bytes);
-    if (jb > 1)
-      mbar_expect_tx(&bars[1], step_bytes);
+    mbar_expect_tx(&bars[1], step_bytes);
+    mbar_expect_tx(&bars[3], (uint32_t)(CS * 4));
+    mbar_expect_tx(&bars[4], (uint32_t)(CS * 4));
+    for (int jj = 0; jj < IB; ++jj)
+      mbar_expect_tx(&bars[5 + jj], (uint32_t)sizeof(S));
   }
+  if (t == 0)
+    cta_beaten = 0;
+  if (t < IB)
+    piv_rank[t] = -1;
   if (multi)
     cluster_sync_all();
   else
@@ -333,7 +347,9 @@ __global__ void __launch_bounds__(NTX, 1)
   long long ptlast = clock64();
 #endif
   T cur[RPT][IB];  // current block columns (registers, static indices)
-  int step = 0;    // global step index j (parity / phase bookkeeping)
+  int step = 0;    // exchange steps so far (inbox parity / phase bookkeeping)
+  int vblk = 0;    // speculative blocks so far (their barriers' phases)
+  int skip = 0, backoff = 0;  // speculation back-off after a beaten block
 #pragma unroll 1
   for (int jb0 = 0; jb0 < jb; jb0 += IB)
   {
@@ -349,18 +365,153 @@ __global__ void __launch_bounds__(NTX, 1)
     const int bend = min(jb0 + IB, jb);  // first column right of the block
     // right-column chunks of one pivot row, from the chunk-aligned jb0 + IB on
     const int rch = (int)(((size_t)(NB - (jb0 + IB)) * sizeof(T) + 15) / 16);
-    if (t < IB)
-      piv_rank[t] = -1;
+    // (piv_rank is reset at the previous block's end / kernel start)
     // Arm the block exchange before this CTA sends any step message of the
     // block: a peer sends block data only after every CTA's last step message.
     if (t == 0 && multi && bend < jb)
       mbar_expect_tx(&bars[2], (uint32_t)((bend - jb0) * rch * 16));
 
+    // ---- speculative block: assume every pivot of the block is the row
+    // already at position k (no row interchange). The row's owner pushes it
+    // to every CTA (one sender, one DSMEM hop per step, no reduction on the
+    // critical path); each CTA checks locally that no row below beats it
+    // (|a| strictly larger, NaN never) and the verdicts are exchanged once
+    // per block. A beaten block is restored and redone with the exchange
+    // steps below -- the result is the reference's either way.
+    bool spec_done = false;
+    const bool try_spec = multi && spec_ok && skip == 0 && jb0 + IB <= jb;
+    if (!try_spec && skip > 0)
+      --skip;
+    if (try_spec)
+    {
+      bool beaten = false;
+      int zj = IB;  // first step whose pivot is exactly zero
+      const uint32_t sph = (uint32_t)(vblk & 1);
+#pragma unroll
+      for (int jj = 0; jj < IB; ++jj)
+      {
+        const int k = k0 + jb0 + jj;
+        bool own = false;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+          if (pos[q] == k)
+          {
+            own = true;
+            const T v = cur[q][jj];
+            const bool vn = is_nan_t(v);
+            S &m = sstage[warp];
+            m.key = vn ? FORCED : mag_key(v);
+            m.pos = k;
+            m.nan = vn ? 1 : 0;
+#pragma unroll
+            for (int c = 0; c < IB; ++c)
+              m.blk[c] = cur[q][c];
+            chosen[q] = jj;
+            piv_rank[jj] = rank;
+            piv_lrow[jj] = t + q * NT;
+          }
+        if (__any_sync(0xffffffffu, own))
+        {
+          __syncwarp();
+          constexpr int NCH = sizeof(S) / 16;
+          const uint4 *src = reinterpret_cast<const uint4 *>(&sstage[warp]);
+          for (int idx = lane; idx < NCH * CS; idx += 32)
+          {
+            const int d = idx / NCH, ch = idx - d * NCH;
+            st_async_v4(mapa(smem_addr(&sinbox[jj]), (uint32_t)d) + ch * 16, src[ch],
+                        mapa(smem_addr(&bars[5 + jj]), (uint32_t)d));
+          }
+        }
+        mbar_wait(&bars[5 + jj], sph);
+        const unsigned long long skey = sinbox[jj].key;
+        const T *Ublk = sinbox[jj].blk;
+        if (!sinbox[jj].nan && skey == 1ull)
+          zj = min(zj, jj);
+        if (t < IB)
+          Ub[jj * NB + jb0 + t] = Ublk[t];
+        const T piv = Ublk[jj];
+        T ub[IB];
+#pragma unroll
+        for (int c = jj + 1; c < IB; ++c)
+          ub[c] = Ublk[c];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+        {
+          if (pos[q] > k)
+          {
+            const T v = cur[q][jj];
+            if (!is_nan_t(v) && mag_key(v) > skey)
+              beaten = true;
+            const T l = divide(v, piv);
+            cur[q][jj] = l;
+#pragma unroll
+            for (int c = jj + 1; c < IB; ++c)
+              cur[q][c] = upd(cur[q][c], l, ub[c]);
+          }
+        }
+      }
+      // verdict exchange (one word per CTA); re-arm this block's barriers
+      // first: no peer can send the next speculative block before it has
+      // this CTA's verdict
+      if (t == 0)
+        for (int jj = 0; jj < IB; ++jj)
+          mbar_expect_tx(&bars[5 + jj], (uint32_t)sizeof(S));
+      if (__any_sync(0xffffffffu, beaten) && lane == 0)
+        cta_beaten = 1;
+      __syncthreads();
+      const int vp = vblk & 1;
+      if (warp == 0 && lane < CS)
+      {
+        const uint32_t v = (uint32_t)cta_beaten;
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                mapa(smem_addr(&vflag[vp][rank]), (uint32_t)lane)),
+            "r"(v), "r"(mapa(smem_addr(&bars[3 + vp]), (uint32_t)lane))
+            : "memory");
+      }
+      mbar_wait(&bars[3 + vp], (uint32_t)((vblk >> 1) & 1));
+      const bool any_beaten =
+          __any_sync(0xffffffffu, lane < CS ? vflag[vp][lane] != 0u : false);
+      ++vblk;
+      __syncthreads();  // everyone has read vflag[vp] and cta_beaten
+      if (t == 0)
+      {
+        mbar_expect_tx(&bars[3 + vp], (uint32_t)(CS * 4));  // for block vblk + 1 (same parity)
+        cta_beaten = 0;
+      }
+      if (!any_beaten)
+      {
+        spec_done = true;
+        backoff = 0;
+        if (rank == 0 && t < IB)
+          ipiv[k0 + jb0 + t] = k0 + jb0 + t;
+        if (rank == 0 && t == 0 && zj < IB)
+          atomicMin(&info->singular_col, k0 + jb0 + zj);
+      }
+      else
+      {
+        // P still holds the block columns as of the block start
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+        {
+          chosen[q] = IB;
+#pragma unroll
+          for (int jj = 0; jj < IB; ++jj)
+            cur[q][jj] = P[(jb0 + jj) * R + t + q * NT];
+        }
+        if (t < IB)
+          piv_rank[t] = -1;
+        backoff = backoff ? min(2 * backoff, 8) : 1;
+        skip = backoff;
+        __syncthreads();  // piv_rank reset before the exchange steps set it
+      }
+    }
+
 #pragma unroll
     for (int jj = 0; jj < IB; ++jj)
     {
       const int j = jb0 + jj;
-      if (j >= jb)
+      if (j >= jb || spec_done)
         break;
       const int k = k0 + j;
       const int par = step & 1;
@@ -464,8 +615,8 @@ __global__ void __launch_bounds__(NTX, 1)
         //    barrier for step+2 (no peer can send step+2 data before every CTA,
         //    this one included, has pushed step+1).
         mbar_wait(&bars[par], (uint32_t)((step >> 1) & 1));
-        if (t == 0 && step + 2 < jb)
-          mbar_expect_tx(&bars[par], step_bytes);
+        if (t == 0)
+          mbar_expect_tx(&bars[par], step_bytes);  // for exchange step + 2
         PT_MARK(5);
         // 7. global winner (identical in every thread of every CTA).
         const unsigned long long gk0 = lane < CS ? inbox[par][lane].key : 0ull;
@@ -590,6 +741,10 @@ __global__ void __launch_bounds__(NTX, 1)
         Ub[jj * NB + c] = u[jj];
     }
     __syncthreads();
+    // piv_rank's last readers are behind this barrier; the next block's first
+    // writers are behind the block's final one
+    if (t < IB)
+      piv_rank[t] = -1;
     PT_MARK(10);
     // (b) every row: its right columns get the updates of the steps at which it
     //     was still below the pivot (all IB for non-pivot rows). Four columns
@@ -650,11 +805,11 @@ __global__ void __launch_bounds__(NTX, 1)
   PT_MARK(8);
 #ifdef MPIRG_DEBUG_PANEL
   if (t == 0 && rank == 0 && (k0 == 0 || k0 + jb >= n))
-    printf("panel k0=%d CS=%d steps=%d cycles/step: cand %lld warp %lld sync %lld cta %lld push %lld "
+    printf("panel k0=%d CS=%d spec_blocks=%d steps=%d cycles/step: cand %lld warp %lld sync %lld cta %lld push %lld "
            "wait %lld glob %lld upd %lld | per panel: (a) %lld (b) %lld | push: wg %lld gather %lld fence %lld\n",
-           k0, CS, step, ptacc[0] / step, ptacc[1] / step, ptacc[2] / step, ptacc[3] / step,
-           ptacc[4] / step, ptacc[5] / step, ptacc[6] / step, ptacc[7] / step, ptacc[10],
-           ptacc[11], ptacc[12] / step, ptacc[13] / step, ptacc[14] / step);
+           k0, CS, vblk, step, ptacc[0] / max(step, 1), ptacc[1] / max(step, 1), ptacc[2] / max(step, 1), ptacc[3] / max(step, 1),
+           ptacc[4] / max(step, 1), ptacc[5] / max(step, 1), ptacc[6] / max(step, 1), ptacc[7] / max(step, 1), ptacc[10],
+           ptacc[11], ptacc[12] / max(step, 1), ptacc[13] / max(step, 1), ptacc[14] / max(step, 1));
 #endif
   // Write every row to its final position; record the row moves.
 #pragma unroll

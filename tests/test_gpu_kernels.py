@@ -179,7 +179,7 @@ def test_lu_antidiagonal_pivots(gpulib):
 
 # ---------------------------------------------------------------- TRSV -----
 @pytest.mark.parametrize("ts,tf", [(B64, B32), (B32, B32), (B32, B16), (B64, B64), (B64, B16)])
-@pytest.mark.parametrize("n", [1, 31, 100, 1025])
+@pytest.mark.parametrize("n", [1, 31, 100, 1025, 2113])
 def test_solve_mps_bitwise(orc, ts, tf, n, gpulib):
     import torch
     a64 = normal_matrix(n, 100 + n) if n > 1 else np.ones((1, 1), order="F")
