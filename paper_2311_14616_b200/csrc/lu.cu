@@ -35,6 +35,7 @@
 #include <climits>
 #include <cstring>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -385,6 +386,151 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
   }
 }
 
+// binary32 trailing update, vectorised (n % 4 == 0, 16-byte aligned A):
+// BM x BN tile of C per CTA of 256 threads (16 x 16), each thread a
+// (BM/16) x (BN/16) micro-tile made of 4-row x 4-column groups 64 apart, so
+// every C access is a float4 along a column (coalesced 256 B per 16 lanes)
+// and every operand read from shared memory is an LDS.128. Same arithmetic
+// and per-element order as lu_gemm_kernel: the accumulator starts from A22
+// and takes one FMA per k, k ascending.
+template <int NB, int BM, int BN>
+__global__ void __launch_bounds__(256, 2) lu_gemm_v4_kernel(float *__restrict__ A, int n, int k0,
+                                                         int jb, int cb, int ce, ColMap map)
+{
+  constexpr int TM = BM / 16, TN = BN / 16;
+  constexpr int BPAD = 4;
+  extern __shared__ __align__(16) unsigned char gsm[];
+  float *As = reinterpret_cast<float *>(gsm);  // [NB][BM]
+  float *Bs = As + (size_t)NB * BM;            // [NB][BN + BPAD]
+  const int c0 = k0 + jb;
+  const int r0 = c0 + blockIdx.x * BM;
+  const int cc0 = cb + blockIdx.y * BN;
+  const int t = threadIdx.x;
+  const int tx = t & 15, ty = t >> 4;
+  {
+    // A block: As[kk][m] = A[(k0+kk)*n + r0 + m], float4 along m
+    constexpr int AV = NB * BM / 4 / 256;
+    float4 ta[AV];
+#pragma unroll
+    for (int u = 0; u < AV; ++u)
+    {
+      const int idx = t + u * 256;
+      const int kk = idx / (BM / 4), m4 = idx % (BM / 4);
+      const int row = r0 + 4 * m4;
+      ta[u] = (kk < jb && row < n)
+                  ? __ldg(reinterpret_cast<const float4 *>(A + (size_t)(k0 + kk) * n + row))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // B block: Bs[kb][nn] = A[col(nn)*n + k0 + kb], float4 along kb
+    constexpr int BV = NB * BN / 4 / 256;
+    float4 tb[BV];
+#pragma unroll
+    for (int u = 0; u < BV; ++u)
+    {
+      const int idx = t + u * 256;
+      const int nn = idx % BN, kq = idx / BN;
+      const int col = cc0 + nn;
+      tb[u] = (col < ce && 4 * kq < jb)
+                  ? __ldg(reinterpret_cast<const float4 *>(A + (size_t)map.g(col) * n + k0 + 4 * kq))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < AV; ++u)
+    {
+      const int idx = t + u * 256;
+      const int kk = idx / (BM / 4), m4 = idx % (BM / 4);
+      reinterpret_cast<float4 *>(As + kk * BM)[m4] = ta[u];
+    }
+#pragma unroll
+    for (int u = 0; u < BV; ++u)
+    {
+      const int idx = t + u * 256;
+      const int nn = idx % BN, kq = idx / BN;
+      // k beyond jb must not contribute: zero the lanes past jb
+      const float v[4] = {tb[u].x, tb[u].y, tb[u].z, tb[u].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        Bs[(4 * kq + e) * (BN + BPAD) + nn] = (4 * kq + e < jb) ? v[e] : 0.f;
+    }
+  }
+
+  float acc[TM][TN];
+#pragma unroll
+  for (int gj = 0; gj < TN / 4; ++gj)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+    {
+      const int col = cc0 + gj * 64 + ty * 4 + j;
+#pragma unroll
+      for (int gi = 0; gi < TM / 4; ++gi)
+      {
+        const int row = r0 + gi * 64 + tx * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < n && col < ce)
+          v = *reinterpret_cast<const float4 *>(A + (size_t)map.g(col) * n + row);
+        acc[gi * 4 + 0][gj * 4 + j] = v.x;
+        acc[gi * 4 + 1][gj * 4 + j] = v.y;
+        acc[gi * 4 + 2][gj * 4 + j] = v.z;
+        acc[gi * 4 + 3][gj * 4 + j] = v.w;
+      }
+    }
+  __syncthreads();
+
+#pragma unroll 4
+  for (int kk = 0; kk < jb; ++kk)
+  {
+    float a[TM], b[TN];
+    const float *ar = As + kk * BM;
+    const float *br = Bs + kk * (BN + BPAD);
+#pragma unroll
+    for (int gi = 0; gi < TM / 4; ++gi)
+    {
+      const float4 v = reinterpret_cast<const float4 *>(ar + gi * 64)[tx];
+      a[gi * 4 + 0] = v.x;
+      a[gi * 4 + 1] = v.y;
+      a[gi * 4 + 2] = v.z;
+      a[gi * 4 + 3] = v.w;
+    }
+#pragma unroll
+    for (int gj = 0; gj < TN / 4; ++gj)
+    {
+      const float4 v = reinterpret_cast<const float4 *>(br + gj * 64)[ty];
+      b[gj * 4 + 0] = v.x;
+      b[gj * 4 + 1] = v.y;
+      b[gj * 4 + 2] = v.z;
+      b[gj * 4 + 3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+        acc[i][j] = __fmaf_rn(-a[i], b[j], acc[i][j]);
+  }
+
+#pragma unroll
+  for (int gj = 0; gj < TN / 4; ++gj)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+    {
+      const int col = cc0 + gj * 64 + ty * 4 + j;
+#pragma unroll
+      for (int gi = 0; gi < TM / 4; ++gi)
+      {
+        const int row = r0 + gi * 64 + tx * 4;
+        if (row < n && col < ce)
+          *reinterpret_cast<float4 *>(A + (size_t)map.g(col) * n + row) =
+              make_float4(acc[gi * 4 + 0][gj * 4 + j], acc[gi * 4 + 1][gj * 4 + j],
+                          acc[gi * 4 + 2][gj * 4 + j], acc[gi * 4 + 3][gj * 4 + j]);
+      }
+    }
+}
+
+template <int NB, int BM, int BN>
+constexpr size_t gemm_v4_smem()
+{
+  return sizeof(float) * ((size_t)NB * BM + (size_t)NB * (BN + 4));
+}
+
 __global__ void iota_kernel(int *p, int n)
 {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -593,14 +739,56 @@ void launch_mt(T *a, int n, int k0, int jb, int cb, int ce, ColMap map, const in
   prof_end(KC_TRSM, s);
 }
 
+template <int NB, int BM, int BN>
+void launch_gemm_v4_t(float *a, int n, int k0, int jb, int cb, int ce, ColMap map, cudaStream_t s)
+{
+  static bool configured = false;
+  if (!configured)
+  {
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_v4_kernel<NB, BM, BN>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)gemm_v4_smem<NB, BM, BN>()));
+    configured = true;
+  }
+  const int c0 = k0 + jb;
+  const dim3 grid((n - c0 + BM - 1) / BM, (ce - cb + BN - 1) / BN);
+  lu_gemm_v4_kernel<NB, BM, BN><<<grid, 256, gemm_v4_smem<NB, BM, BN>(), s>>>(a, n, k0, jb, cb,
+                                                                              ce, map);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+// MPIRG_GEMM=scalar forces the generic kernel (A/B measurements).
+static bool gemm_v4_allowed()
+{
+  static const bool v = [] {
+    const char *e = std::getenv("MPIRG_GEMM");
+    return !(e && std::string(e) == "scalar");
+  }();
+  return v;
+}
+
 template <typename T, int NB>
 void launch_gemm(T *a, int n, int k0, int jb, int cb, int ce, ColMap map, cudaStream_t s)
 {
   const int c0 = k0 + jb;
   if (ce <= cb || c0 >= n)
     return;
-  configure_gemm<T, NB>();
   prof_begin(KC_GEMM, s);
+  if constexpr (std::is_same<T, float>::value && NB >= 16)
+  {
+    if (n % 4 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0 && gemm_v4_allowed())
+    {
+      // 128 x 128 tiles while they fill the GPU twice over, else 64 x 64
+      const long tiles128 = (long)((n - c0 + 127) / 128) * ((ce - cb + 127) / 128);
+      if (tiles128 >= 2 * 148)
+        launch_gemm_v4_t<NB, 128, 128>(a, n, k0, jb, cb, ce, map, s);
+      else
+        launch_gemm_v4_t<NB, 64, 64>(a, n, k0, jb, cb, ce, map, s);
+      prof_end(KC_GEMM, s);
+      return;
+    }
+  }
+  configure_gemm<T, NB>();
   const dim3 grid((n - c0 + GB - 1) / GB, (ce - cb + GB - 1) / GB);
   lu_gemm_kernel<T, NB><<<grid, 256, gemm_smem_bytes<T, NB>(), s>>>(a, n, k0, jb, cb, ce, map);
   MPIRG_CUDA_CHECK(cudaGetLastError());

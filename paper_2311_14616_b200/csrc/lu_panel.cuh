@@ -422,7 +422,9 @@ __global__ void __launch_bounds__(NTX, 1)
                         mapa(smem_addr(&bars[5 + jj]), (uint32_t)d));
           }
         }
+        PT_MARK(12);
         mbar_wait(&bars[5 + jj], sph);
+        PT_MARK(13);
         const unsigned long long skey = sinbox[jj].key;
         const T *Ublk = sinbox[jj].blk;
         if (!sinbox[jj].nan && skey == 1ull)
@@ -450,6 +452,7 @@ __global__ void __launch_bounds__(NTX, 1)
           }
         }
       }
+      PT_MARK(14);
       // verdict exchange (one word per CTA); re-arm this block's barriers
       // first: no peer can send the next speculative block before it has
       // this CTA's verdict
@@ -479,6 +482,7 @@ __global__ void __launch_bounds__(NTX, 1)
         mbar_expect_tx(&bars[3 + vp], (uint32_t)(CS * 4));  // for block vblk + 1 (same parity)
         cta_beaten = 0;
       }
+      PT_MARK(15);
       if (!any_beaten)
       {
         spec_done = true;
@@ -806,10 +810,10 @@ __global__ void __launch_bounds__(NTX, 1)
 #ifdef MPIRG_DEBUG_PANEL
   if (t == 0 && rank == 0 && (k0 == 0 || k0 + jb >= n))
     printf("panel k0=%d CS=%d spec_blocks=%d steps=%d cycles/step: cand %lld warp %lld sync %lld cta %lld push %lld "
-           "wait %lld glob %lld upd %lld | per panel: (a) %lld (b) %lld | push: wg %lld gather %lld fence %lld\n",
+           "wait %lld glob %lld upd %lld | per panel: (a) %lld (b) %lld | spec per step: push %lld wait %lld upd %lld; verdict/blk %lld\n",
            k0, CS, vblk, step, ptacc[0] / max(step, 1), ptacc[1] / max(step, 1), ptacc[2] / max(step, 1), ptacc[3] / max(step, 1),
            ptacc[4] / max(step, 1), ptacc[5] / max(step, 1), ptacc[6] / max(step, 1), ptacc[7] / max(step, 1), ptacc[10],
-           ptacc[11], ptacc[12] / max(step, 1), ptacc[13] / max(step, 1), ptacc[14] / max(step, 1));
+           ptacc[11], ptacc[12] / max(8 * vblk, 1), ptacc[13] / max(8 * vblk, 1), ptacc[14] / max(8 * vblk, 1), ptacc[15] / max(vblk, 1));
 #endif
   // Write every row to its final position; record the row moves.
 #pragma unroll
