@@ -52,6 +52,16 @@ struct alignas(16) Slot
   T blk[IB];               // the candidate's block columns, as of this step
 };
 
+// Speculative block message: the block's IB finished pivot rows (block
+// columns) and whether the block's natural rows were in place.
+template <typename T>
+struct alignas(16) BMsg
+{
+  T blk[IB][IB];
+  uint32_t flag;
+  uint32_t pad[3];
+};
+
 // Warp-level candidate staged for the CTA reduction.
 template <typename T>
 struct alignas(16) WSlot
@@ -259,9 +269,9 @@ __global__ void __launch_bounds__(NTX, 1)
   __shared__ S inbox[2][MAXCS];      // every CTA's candidate (st.async from the peers)
   // [0],[1]: exchange-step inboxes, [2]: block exchange, [3],[4]: block
   // verification flags, [5 + jj]: speculative step jj of a block
-  __shared__ __align__(8) uint64_t bars[5 + IB];
-  __shared__ S sinbox[IB];                 // speculative pivot rows (one sender per step)
-  __shared__ S sstage[NW];                 // the sending warp's staged message
+  __shared__ __align__(8) uint64_t bars[6];
+  __shared__ BMsg<T> binbox;               // speculative block: its IB pivot rows
+  __shared__ BMsg<T> bstage;               // the owner warp's staged message
   __shared__ uint32_t vflag[2][MAXCS];     // every CTA's "speculation beaten" flag
   __shared__ int cta_beaten;
   __shared__ int piv_rank[IB], piv_lrow[IB];  // owner CTA / local row of the block's pivots
@@ -303,17 +313,16 @@ __global__ void __launch_bounds__(NTX, 1)
   const uint32_t step_bytes = (uint32_t)(CS * sizeof(S));
   if (t == 0 && multi)
   {
-    for (int i = 0; i < 5 + IB; ++i)
+    for (int i = 0; i < 6; ++i)
       mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // Arm every first phase before any peer can send: the exchange steps'
-    // two parities, both verification parities, each speculative step.
+    // two parities, both verdict parities, the speculative block message.
     mbar_expect_tx(&bars[0], step_bytes);
     mbar_expect_tx(&bars[1], step_bytes);
     mbar_expect_tx(&bars[3], (uint32_t)(CS * 4));
     mbar_expect_tx(&bars[4], (uint32_t)(CS * 4));
-    for (int jj = 0; jj < IB; ++jj)
-      mbar_expect_tx(&bars[5 + jj], (uint32_t)sizeof(S));
+    mbar_expect_tx(&bars[5], (uint32_t)sizeof(BMsg<T>));
   }
   if (t == 0)
     cta_beaten = 0;
@@ -348,7 +357,8 @@ __global__ void __launch_bounds__(NTX, 1)
 #endif
   T cur[RPT][IB];  // current block columns (registers, static indices)
   int step = 0;    // exchange steps so far (inbox parity / phase bookkeeping)
-  int vblk = 0;    // speculative blocks so far (their barriers' phases)
+  int vblk = 0;    // speculative block messages so far (bars[5] phase)
+  int nverd = 0;   // verdict exchanges so far (bars[3 + parity] phases)
   int skip = 0, backoff = 0;  // speculation back-off after a beaten block
 #pragma unroll 1
   for (int jb0 = 0; jb0 < jb; jb0 += IB)
@@ -372,142 +382,185 @@ __global__ void __launch_bounds__(NTX, 1)
       mbar_expect_tx(&bars[2], (uint32_t)((bend - jb0) * rch * 16));
 
     // ---- speculative block: assume every pivot of the block is the row
-    // already at position k (no row interchange). The row's owner pushes it
-    // to every CTA (one sender, one DSMEM hop per step, no reduction on the
-    // critical path); each CTA checks locally that no row below beats it
-    // (|a| strictly larger, NaN never) and the verdicts are exchanged once
-    // per block. A beaten block is restored and redone with the exchange
-    // steps below -- the result is the reference's either way.
+    // already at position k (no row interchange). The CTA that naturally
+    // holds positions [k, k+IB) factors those IB rows among themselves (a
+    // small LU on IB lanes of one warp) and pushes the IB finished pivot rows
+    // to every CTA in ONE message; every CTA then runs the block's IB steps
+    // locally, checking that no row below a pivot beats it (|a| strictly
+    // larger; NaN never), and the verdicts are exchanged once per block. A
+    // beaten block is restored and redone with the exchange steps below --
+    // the result is the reference's either way. If the natural rows are not
+    // in place (an earlier interchange moved them) the message says so and
+    // the block takes the exchange steps directly.
     bool spec_done = false;
     const bool try_spec = multi && spec_ok && skip == 0 && jb0 + IB <= jb;
     if (!try_spec && skip > 0)
       --skip;
     if (try_spec)
     {
-      bool beaten = false;
-      int zj = IB;  // first step whose pivot is exactly zero
-      const uint32_t sph = (uint32_t)(vblk & 1);
-#pragma unroll
-      for (int jj = 0; jj < IB; ++jj)
+      const int kb = k0 + jb0;                   // first position of the block
+      const int orank = (kb - k0) / R;           // CTA naturally holding [kb, kb+IB)
+      const int oidx = kb - k0 - orank * R;      // = t0 + q0 * NT
+      const int t0 = oidx % NT, q0 = oidx / NT;
+      if (rank == orank && warp == t0 / 32)
       {
-        const int k = k0 + jb0 + jj;
-        bool own = false;
+        const int li = lane - (t0 & 31);  // 0..IB-1 on the block's lanes
+        const bool mine = li >= 0 && li < IB;
+        T rv[IB];
+        bool inplace = false;
 #pragma unroll
         for (int q = 0; q < RPT; ++q)
-          if (pos[q] == k)
+          if (q == q0)
           {
-            own = true;
-            const T v = cur[q][jj];
-            const bool vn = is_nan_t(v);
-            S &m = sstage[warp];
-            m.key = vn ? FORCED : mag_key(v);
-            m.pos = k;
-            m.nan = vn ? 1 : 0;
 #pragma unroll
             for (int c = 0; c < IB; ++c)
-              m.blk[c] = cur[q][c];
-            chosen[q] = jj;
-            piv_rank[jj] = rank;
-            piv_lrow[jj] = t + q * NT;
+              rv[c] = cur[q][c];
+            inplace = mine && pos[q] == kb + li;
           }
-        if (__any_sync(0xffffffffu, own))
+        const bool clean = __popc(__ballot_sync(0xffffffffu, inplace)) == IB;
+        if (clean)
         {
-          __syncwarp();
-          constexpr int NCH = sizeof(S) / 16;
-          const uint4 *src = reinterpret_cast<const uint4 *>(&sstage[warp]);
-          for (int idx = lane; idx < NCH * CS; idx += 32)
-          {
-            const int d = idx / NCH, ch = idx - d * NCH;
-            st_async_v4(mapa(smem_addr(&sinbox[jj]), (uint32_t)d) + ch * 16, src[ch],
-                        mapa(smem_addr(&bars[5 + jj]), (uint32_t)d));
-          }
-        }
-        PT_MARK(12);
-        mbar_wait(&bars[5 + jj], sph);
-        PT_MARK(13);
-        const unsigned long long skey = sinbox[jj].key;
-        const T *Ublk = sinbox[jj].blk;
-        if (!sinbox[jj].nan && skey == 1ull)
-          zj = min(zj, jj);
-        if (t < IB)
-          Ub[jj * NB + jb0 + t] = Ublk[t];
-        const T piv = Ublk[jj];
-        T ub[IB];
-#pragma unroll
-        for (int c = jj + 1; c < IB; ++c)
-          ub[c] = Ublk[c];
-#pragma unroll
-        for (int q = 0; q < RPT; ++q)
-        {
-          if (pos[q] > k)
-          {
-            const T v = cur[q][jj];
-            if (!is_nan_t(v) && mag_key(v) > skey)
-              beaten = true;
-            const T l = divide(v, piv);
-            cur[q][jj] = l;
-#pragma unroll
-            for (int c = jj + 1; c < IB; ++c)
-              cur[q][c] = upd(cur[q][c], l, ub[c]);
-          }
-        }
-      }
-      PT_MARK(14);
-      // verdict exchange (one word per CTA); re-arm this block's barriers
-      // first: no peer can send the next speculative block before it has
-      // this CTA's verdict
-      if (t == 0)
-        for (int jj = 0; jj < IB; ++jj)
-          mbar_expect_tx(&bars[5 + jj], (uint32_t)sizeof(S));
-      if (__any_sync(0xffffffffu, beaten) && lane == 0)
-        cta_beaten = 1;
-      __syncthreads();
-      const int vp = vblk & 1;
-      if (warp == 0 && lane < CS)
-      {
-        const uint32_t v = (uint32_t)cta_beaten;
-        asm volatile(
-            "st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
-                mapa(smem_addr(&vflag[vp][rank]), (uint32_t)lane)),
-            "r"(v), "r"(mapa(smem_addr(&bars[3 + vp]), (uint32_t)lane))
-            : "memory");
-      }
-      mbar_wait(&bars[3 + vp], (uint32_t)((vblk >> 1) & 1));
-      const bool any_beaten =
-          __any_sync(0xffffffffu, lane < CS ? vflag[vp][lane] != 0u : false);
-      ++vblk;
-      __syncthreads();  // everyone has read vflag[vp] and cta_beaten
-      if (t == 0)
-      {
-        mbar_expect_tx(&bars[3 + vp], (uint32_t)(CS * 4));  // for block vblk + 1 (same parity)
-        cta_beaten = 0;
-      }
-      PT_MARK(15);
-      if (!any_beaten)
-      {
-        spec_done = true;
-        backoff = 0;
-        if (rank == 0 && t < IB)
-          ipiv[k0 + jb0 + t] = k0 + jb0 + t;
-        if (rank == 0 && t == 0 && zj < IB)
-          atomicMin(&info->singular_col, k0 + jb0 + zj);
-      }
-      else
-      {
-        // P still holds the block columns as of the block start
-#pragma unroll
-        for (int q = 0; q < RPT; ++q)
-        {
-          chosen[q] = IB;
+          // IB-step LU of the block's pivot rows (reference order per element)
 #pragma unroll
           for (int jj = 0; jj < IB; ++jj)
-            cur[q][jj] = P[(jb0 + jj) * R + t + q * NT];
+          {
+            T u[IB];
+#pragma unroll
+            for (int c = jj; c < IB; ++c)
+              u[c] = shfl_t(rv[c], (t0 & 31) + jj);
+            if (mine && li > jj)
+            {
+              const T l = divide(rv[jj], u[jj]);
+              rv[jj] = l;
+#pragma unroll
+              for (int c = jj + 1; c < IB; ++c)
+                rv[c] = upd(rv[c], l, u[c]);
+            }
+          }
+          if (mine)
+          {
+#pragma unroll
+            for (int c = 0; c < IB; ++c)
+              bstage.blk[li][c] = rv[c];
+          }
         }
-        if (t < IB)
-          piv_rank[t] = -1;
-        backoff = backoff ? min(2 * backoff, 8) : 1;
-        skip = backoff;
-        __syncthreads();  // piv_rank reset before the exchange steps set it
+        if (lane == 0)
+          bstage.flag = clean ? 1u : 0u;
+        __syncwarp();
+        constexpr int NCH = sizeof(BMsg<T>) / 16;
+        const uint4 *src = reinterpret_cast<const uint4 *>(&bstage);
+        const uint32_t dst0 = smem_addr(&binbox), bar0 = smem_addr(&bars[5]);
+        for (int idx = lane; idx < NCH * CS; idx += 32)
+        {
+          const int d = idx / NCH, ch = idx - d * NCH;
+          st_async_v4(mapa(dst0, (uint32_t)d) + ch * 16, src[ch], mapa(bar0, (uint32_t)d));
+        }
+      }
+      PT_MARK(12);
+      mbar_wait(&bars[5], (uint32_t)(vblk & 1));
+      PT_MARK(13);
+      // re-arm for the next block message: its sender must first pass this
+      // block's verdict exchange or exchange steps, which need this CTA
+      if (t == 0)
+        mbar_expect_tx(&bars[5], (uint32_t)sizeof(BMsg<T>));
+      const bool clean = binbox.flag != 0u;
+      ++vblk;
+      if (clean)
+      {
+        bool beaten = false;
+        int zj = IB;  // first step whose pivot is exactly zero
+#pragma unroll
+        for (int jj = 0; jj < IB; ++jj)
+        {
+          const int k = kb + jj;
+          const T piv = binbox.blk[jj][jj];
+          const bool pnan = is_nan_t(piv);
+          const unsigned long long skey = pnan ? FORCED : mag_key(piv);
+          if (!pnan && skey == 1ull)
+            zj = min(zj, jj);
+          if (t < IB)
+            Ub[jj * NB + jb0 + t] = binbox.blk[jj][t];
+          T ub[IB];
+#pragma unroll
+          for (int c = jj + 1; c < IB; ++c)
+            ub[c] = binbox.blk[jj][c];
+#pragma unroll
+          for (int q = 0; q < RPT; ++q)
+          {
+            if (pos[q] == k)
+            {
+#pragma unroll
+              for (int c = 0; c < IB; ++c)
+                cur[q][c] = binbox.blk[jj][c];
+              chosen[q] = jj;
+              piv_rank[jj] = rank;
+              piv_lrow[jj] = t + q * NT;
+            }
+            else if (pos[q] > k)
+            {
+              const T v = cur[q][jj];
+              if (!is_nan_t(v) && mag_key(v) > skey)
+                beaten = true;
+              const T l = divide(v, piv);
+              cur[q][jj] = l;
+#pragma unroll
+              for (int c = jj + 1; c < IB; ++c)
+                cur[q][c] = upd(cur[q][c], l, ub[c]);
+            }
+          }
+        }
+        PT_MARK(14);
+        // verdict exchange (one word per CTA)
+        if (__any_sync(0xffffffffu, beaten) && lane == 0)
+          cta_beaten = 1;
+        __syncthreads();
+        const int vp = nverd & 1;
+        if (warp == 0 && lane < CS)
+        {
+          const uint32_t v = (uint32_t)cta_beaten;
+          asm volatile(
+              "st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                  mapa(smem_addr(&vflag[vp][rank]), (uint32_t)lane)),
+              "r"(v), "r"(mapa(smem_addr(&bars[3 + vp]), (uint32_t)lane))
+              : "memory");
+        }
+        mbar_wait(&bars[3 + vp], (uint32_t)((nverd >> 1) & 1));
+        ++nverd;
+        const bool any_beaten =
+            __any_sync(0xffffffffu, lane < CS ? vflag[vp][lane] != 0u : false);
+        __syncthreads();  // everyone has read vflag[vp] and cta_beaten
+        if (t == 0)
+        {
+          mbar_expect_tx(&bars[3 + vp], (uint32_t)(CS * 4));  // for the verdict two blocks on
+          cta_beaten = 0;
+        }
+        PT_MARK(15);
+        if (!any_beaten)
+        {
+          spec_done = true;
+          backoff = 0;
+          if (rank == 0 && t < IB)
+            ipiv[kb + t] = kb + t;
+          if (rank == 0 && t == 0 && zj < IB)
+            atomicMin(&info->singular_col, kb + zj);
+        }
+        else
+        {
+          // P still holds the block columns as of the block start
+#pragma unroll
+          for (int q = 0; q < RPT; ++q)
+          {
+            chosen[q] = IB;
+#pragma unroll
+            for (int jj = 0; jj < IB; ++jj)
+              cur[q][jj] = P[(jb0 + jj) * R + t + q * NT];
+          }
+          if (t < IB)
+            piv_rank[t] = -1;
+          backoff = backoff ? min(2 * backoff, 8) : 1;
+          skip = backoff;
+          __syncthreads();  // piv_rank reset before the exchange steps set it
+        }
       }
     }
 
@@ -810,10 +863,10 @@ __global__ void __launch_bounds__(NTX, 1)
 #ifdef MPIRG_DEBUG_PANEL
   if (t == 0 && rank == 0 && (k0 == 0 || k0 + jb >= n))
     printf("panel k0=%d CS=%d spec_blocks=%d steps=%d cycles/step: cand %lld warp %lld sync %lld cta %lld push %lld "
-           "wait %lld glob %lld upd %lld | per panel: (a) %lld (b) %lld | spec per step: push %lld wait %lld upd %lld; verdict/blk %lld\n",
+           "wait %lld glob %lld upd %lld | per panel: (a) %lld (b) %lld | spec per blk: owner+push %lld wait %lld local %lld verdict %lld\n",
            k0, CS, vblk, step, ptacc[0] / max(step, 1), ptacc[1] / max(step, 1), ptacc[2] / max(step, 1), ptacc[3] / max(step, 1),
            ptacc[4] / max(step, 1), ptacc[5] / max(step, 1), ptacc[6] / max(step, 1), ptacc[7] / max(step, 1), ptacc[10],
-           ptacc[11], ptacc[12] / max(8 * vblk, 1), ptacc[13] / max(8 * vblk, 1), ptacc[14] / max(8 * vblk, 1), ptacc[15] / max(vblk, 1));
+           ptacc[11], ptacc[12] / max(vblk, 1), ptacc[13] / max(vblk, 1), ptacc[14] / max(vblk, 1), ptacc[15] / max(vblk, 1));
 #endif
   // Write every row to its final position; record the row moves.
 #pragma unroll
