@@ -329,8 +329,9 @@ def run_ours(args, world, rank, local):
     ffma = C.c_double(0.0)
     ffma_ms = C.c_double(0.0)
     lib.mpirg_ffma_peak(C.byref(ffma), C.byref(ffma_ms))
-    nb = (64 if n <= 4096 else (32 if n <= 8192 else 16)) if tf == 0 else \
-        (64 if n <= 8192 else 32)
+    # panel width as chosen by lu_choose_nb (lu.cu): binary64 factors narrow
+    # with n, binary32/16 factors use 64 at every n
+    nb = (64 if n <= 4096 else (32 if n <= 8192 else 16)) if tf == 0 else 64
     work = lu_work(n, nb)
     tf_b, tw_b = ESZ[tf], ESZ[tw]
     tc = args.lu_mode == "tc" and tf == 2
