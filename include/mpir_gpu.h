@@ -303,6 +303,11 @@ int mpirg_ffma_peak(double *tflops, double *ms);
 /* The same for binary64 DFMA (the roofline denominator of the fp64 chains:
  * residual and one-norm at small n, where rows/columns < lanes x SMSPs). */
 int mpirg_dfma_peak(double *tflops, double *ms);
+/* Diagnostics: the binary32 trailing update (lu_f32.cuh gemm_tma_kernel) of
+ * rows/columns [K, n) by K <= 128 steps on a zeroed n x n matrix, tile edge
+ * `tile` (128, 64, or 0 = the LU's own choice), averaged over `reps` launches;
+ * *tflops counts 2 (n-K)^2 K flops per launch. */
+int mpirg_ubench_gemm_f32(int n, int K, int tile, int reps, double *tflops, double *ms);
 /* Diagnostics: compares the reciprocal-based division used on the back
  * substitution's critical path (common.cuh div_rcp) with IEEE div.rn on
  * `count` seeded operand pairs of precision `prec` (MPIRG_B64 / MPIRG_B32);

@@ -158,6 +158,8 @@ PROTOTYPES = {
     "mpirg_profile_enable": (None, [_I]),
     "mpirg_profile_collect": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_int), _I]),
     "mpirg_ffma_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "mpirg_ubench_gemm_f32": (_I, [_I, _I, _I, _I, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double)]),
     "mpirg_dfma_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "mpirg_check_fast_div": (_I, [C.c_int, C.c_ulonglong, C.c_longlong,
                                   C.POINTER(C.c_longlong), C.POINTER(C.c_double)]),

@@ -71,6 +71,7 @@ struct LuWorkspace
   int *pp = nullptr;      // [n] composed row map of a tall panel
   int2 *smv = nullptr;    // [2*nb] row moves of the tall panel's 8-column leaves
   int *snm = nullptr;     // [nb/8]
+  void *ut = nullptr;     // float[2*nb][n]: transposed U12 of two steps (binary32)
 };
 // Chooses the panel width for n and the factor precision (0 = auto).
 int lu_choose_nb(int prec, int n, int requested);

@@ -39,7 +39,10 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "../../include/mpir_gpu.h"
+#include "lu_f32.cuh"
 #include "lu_panel.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -873,7 +876,7 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
 {
   const ColMap id{};
   cudaStream_t side = static_cast<cudaStream_t>(ws.side);
-  cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);  // [3][npanels]: P, N, R
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);  // [4][npanels]: P, N, R, F
   const int np = ws.npanels;
   if (perm)
   {
@@ -890,15 +893,17 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
     const int c0 = k0 + jb;
     int2 *mv = ws.moves + (size_t)p * 2 * NB;
     int *nm = ws.nmoves + p;
-    cudaEvent_t evP = ev[p], evN = ev[np + p], evR = ev[2 * np + p];
+    cudaEvent_t evP = ev[p], evN = ev[np + p], evR = ev[2 * np + p], evF = ev[3 * np + p];
     // main: the critical chain
     panel_any<T, NB>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
     MPIRG_CUDA_CHECK(cudaEventRecord(evP, s));
     const int cnext = std::min(n, c0 + NB);
     if (c0 < n)
     {
+      // depth-2 look-ahead: wait only for step p-1's update of these columns
+      // (issued first on the side stream), not for the whole of step p-1
       if (p > 0)
-        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + p - 1], 0));
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[3 * np + p - 1], 0));
       launch_mt<T, NB>(a, n, k0, jb, c0, cnext, id, mv, nm, s);
       trailing_update<T, NB>(a, n, k0, jb, c0, cnext, tc, s);
     }
@@ -907,11 +912,210 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
     MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, evP, 0));
     if (cnext < n)
     {
-      launch_mt<T, NB>(a, n, k0, jb, cnext, n, id, mv, nm, side);
-      trailing_update<T, NB>(a, n, k0, jb, cnext, n, tc, side);
+      // the next panel's columns first: panel p+1's critical chain needs
+      // only these (evF), the bulk of the update then overlaps panel p+1
+      const int cnn = std::min(n, cnext + NB);
+      launch_mt<T, NB>(a, n, k0, jb, cnext, cnn, id, mv, nm, side);
+      trailing_update<T, NB>(a, n, k0, jb, cnext, cnn, tc, side);
+      MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
+      if (cnn < n)
+      {
+        launch_mt<T, NB>(a, n, k0, jb, cnn, n, id, mv, nm, side);
+        trailing_update<T, NB>(a, n, k0, jb, cnn, n, tc, side);
+      }
     }
+    else
+      MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
     launch_moves<T, NB>(a, n, 0, k0, id, mv, nm, perm, side);
     MPIRG_CUDA_CHECK(cudaEventRecord(evR, side));
+  }
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + np - 1], 0));
+}
+
+// ---- binary32 single-GPU schedule: TMA trailing update, paired steps ------
+// MPIRG_GEMM=v4 keeps the one-step-per-pass schedule of lu_run (A/B runs).
+static int f32_mode()
+{
+  static const int v = [] {
+    const char *e = std::getenv("MPIRG_GEMM");
+    if (e && (std::string(e) == "v4" || std::string(e) == "scalar"))
+      return 0;
+    return 1;
+  }();
+  return v;
+}
+
+struct F32Plan
+{
+  CUtensorMap a128, u128, a64, u64;
+  float *a = nullptr, *ut = nullptr;
+  int n = 0;
+};
+
+static void f32_encode(CUtensorMap *map, float *base, int inner, int outer, int box0)
+{
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)inner * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)f32u::GKC};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = tma_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed for the fp32 trailing update");
+}
+
+static void f32_plan_make(F32Plan &p, float *a, int n, float *ut, int ut_rows)
+{
+  p.a = a;
+  p.n = n;
+  p.ut = ut;
+  f32_encode(&p.a128, a, n, n, 128);
+  f32_encode(&p.a64, a, n, n, 64);
+  f32_encode(&p.u128, ut, n, ut_rows, 128);
+  f32_encode(&p.u64, ut, n, ut_rows, 64);
+}
+
+template <int NB>
+static void f32_mt(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 *mv,
+                   const int *nm, int kp, int ut_row, cudaStream_t s)
+{
+  if (ce <= cb)
+    return;
+  prof_begin(KC_TRSM, s);
+  const int g = (ce - cb + f32u::MT_COLS - 1) / f32u::MT_COLS;
+  if (kp >= 0)
+    f32u::mt2_kernel<NB, true><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, kp, P.ut,
+                                                ut_row);
+  else
+    f32u::mt2_kernel<NB, false><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, 0, P.ut,
+                                                 ut_row);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+  prof_end(KC_TRSM, s);
+}
+
+template <int BM>
+static void f32_gemm_t(const CUtensorMap &ma, const CUtensorMap &mu, const F32Plan &P, int k0,
+                       int K, int ut_row, int cb, int ce, cudaStream_t s)
+{
+  static bool configured = false;
+  if (!configured)
+  {
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::gemm_tma_kernel<BM>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)f32u::gemm_tma_smem<BM>()));
+    configured = true;
+  }
+  const int c0 = k0 + K;
+  const dim3 grid((P.n - c0 + BM - 1) / BM, (ce - cb + BM - 1) / BM);
+  f32u::gemm_tma_kernel<BM><<<grid, 256, f32u::gemm_tma_smem<BM>(), s>>>(ma, mu, P.a, P.n, k0,
+                                                                        K, ut_row, cb, ce);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+// rows [k0 + K, n) x columns [cb, ce) -= L(:, k0 .. k0+K) U(k0 .. k0+K, :), U from ut rows
+// [ut_row, ut_row + K)
+static void f32_gemm(const F32Plan &P, int k0, int K, int ut_row, int cb, int ce, cudaStream_t s)
+{
+  const int c0 = k0 + K;
+  if (ce <= cb || c0 >= P.n)
+    return;
+  prof_begin(KC_GEMM, s);
+  const long tiles128 = (long)((P.n - c0 + 127) / 128) * ((ce - cb + 127) / 128);
+  if (tiles128 >= 2 * 148)
+    f32_gemm_t<128>(P.a128, P.u128, P, k0, K, ut_row, cb, ce, s);
+  else
+    f32_gemm_t<64>(P.a64, P.u64, P, k0, K, ut_row, cb, ce, s);
+  prof_end(KC_GEMM, s);
+}
+
+// Same dependency structure as lu_run (critical chain on s, bulk on the side
+// stream), plus pairing: an even step p whose far columns [c0 + 2nb, n) are
+// not needed by the next panel only solves their U12 rows; the odd step p+1
+// then applies its row moves to them and to panel p's L columns, the pending
+// step-p update of its own panel rows (inside the U12 solve), and one K = 2nb
+// update (lu_f32.cuh explains why the bits are unchanged).
+template <int NB>
+void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                cudaStream_t s)
+{
+  const ColMap id{};
+  cudaStream_t side = static_cast<cudaStream_t>(ws.side);
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);  // [4][npanels]: P, N, R, F
+  const int np = ws.npanels;
+  F32Plan P;
+  f32_plan_make(P, a, n, static_cast<float *>(ws.ut), 2 * NB);
+  if (perm)
+  {
+    ProfScope ps(KC_VEC, s);
+    iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(perm, n);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  }
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(ws.nmoves, 0, sizeof(int) * np, s));
+  MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, ev[0], 0));
+  bool prev_deferred = false;
+  for (int p = 0, k0 = 0; k0 < n; ++p, k0 += NB)
+  {
+    const int jb = std::min(NB, n - k0);
+    const int c0 = k0 + jb;
+    const int cnext = std::min(n, c0 + NB);
+    const int cnn = std::min(n, cnext + NB);
+    const int ur = (p & 1) * NB;  // this step's rows of ut
+    int2 *mv = ws.moves + (size_t)p * 2 * NB;
+    int *nm = ws.nmoves + p;
+    cudaEvent_t evP = ev[p], evN = ev[np + p], evR = ev[2 * np + p], evF = ev[3 * np + p];
+    const bool pend = prev_deferred;  // step p-1 left its far-column update to this step
+    const bool defer = !pend && (p & 1) == 0 && cnn < n && jb == NB;
+    const int kp = k0 - NB;
+    panel_any<float, NB>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
+    MPIRG_CUDA_CHECK(cudaEventRecord(evP, s));
+    if (c0 < n)
+    {
+      if (p > 0)
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[3 * np + p - 1], 0));
+      f32_mt<NB>(P, k0, jb, c0, cnext, mv, nm, -1, ur, s);
+      f32_gemm(P, k0, jb, ur, c0, cnext, s);
+    }
+    MPIRG_CUDA_CHECK(cudaEventRecord(evN, s));
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, evP, 0));
+    if (pend)  // panel p-1's L rows follow this step's row moves before they are used
+      launch_moves<float, NB>(a, n, kp, k0, id, mv, nm, nullptr, side);
+    if (cnext < n)
+    {
+      if (pend)
+      {
+        f32_mt<NB>(P, k0, jb, cnext, cnn, mv, nm, kp, ur, side);
+        f32_gemm(P, kp, NB + jb, 0, cnext, cnn, side);
+      }
+      else
+      {
+        f32_mt<NB>(P, k0, jb, cnext, cnn, mv, nm, -1, ur, side);
+        f32_gemm(P, k0, jb, ur, cnext, cnn, side);
+      }
+      MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
+      if (cnn < n)
+      {
+        if (pend)
+        {
+          f32_mt<NB>(P, k0, jb, cnn, n, mv, nm, kp, ur, side);
+          f32_gemm(P, kp, NB + jb, 0, cnn, n, side);
+        }
+        else
+        {
+          f32_mt<NB>(P, k0, jb, cnn, n, mv, nm, -1, ur, side);
+          if (!defer)
+            f32_gemm(P, k0, jb, ur, cnn, n, side);
+        }
+      }
+    }
+    else
+      MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
+    launch_moves<float, NB>(a, n, 0, pend ? kp : k0, id, mv, nm, perm, side);
+    MPIRG_CUDA_CHECK(cudaEventRecord(evR, side));
+    prev_deferred = defer;
   }
   MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + np - 1], 0));
 }
@@ -999,6 +1203,8 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.pp, sizeof(int) * (size_t)std::max(1, n)));
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.smv, sizeof(int2) * 2 * (size_t)ws.nb));
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.snm, sizeof(int) * (size_t)ws.nb));
+  if (prec == B32 && ws.nb == 64 && n % 4 == 0)  // transposed U12 of two steps (lu_run_f32)
+    MPIRG_CUDA_CHECK(cudaMalloc(&ws.ut, sizeof(float) * 2 * (size_t)ws.nb * n));
   cudaStream_t side;
   // The side stream carries the bulk trailing update; give it the lowest
   // priority so the block scheduler hands freed SMs to the critical chain
@@ -1007,8 +1213,8 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
   ws.side = side;
-  auto *ev = new cudaEvent_t[3 * (size_t)ws.npanels];
-  for (int i = 0; i < 3 * ws.npanels; ++i)
+  auto *ev = new cudaEvent_t[4 * (size_t)ws.npanels];
+  for (int i = 0; i < 4 * ws.npanels; ++i)
     MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
   ws.events = ev;
 }
@@ -1016,13 +1222,13 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
 void lu_workspace_free(LuWorkspace &ws)
 {
   for (void *p : {(void *)ws.moves, (void *)ws.nmoves, (void *)ws.pp, (void *)ws.smv,
-                  (void *)ws.snm})
+                  (void *)ws.snm, ws.ut})
     if (p)
       cudaFree(p);
   if (ws.events)
   {
     auto *ev = static_cast<cudaEvent_t *>(ws.events);
-    for (int i = 0; i < 3 * ws.npanels; ++i)
+    for (int i = 0; i < 4 * ws.npanels; ++i)
       cudaEventDestroy(ev[i]);
     delete[] ev;
   }
@@ -1035,6 +1241,15 @@ template <typename T>
 void lu_dispatch(int nb, T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
                  cudaStream_t s, const TcPlan *tc = nullptr)
 {
+  if constexpr (std::is_same<T, float>::value)
+  {
+    if (nb == 64 && f32_mode() && ws.ut && n % 4 == 0 &&
+        reinterpret_cast<uintptr_t>(a) % 16 == 0)
+    {
+      lu_run_f32<64>(a, n, ipiv, perm, ws, info, s);
+      return;
+    }
+  }
   if (nb == 64)
     lu_run<T, 64>(a, n, ipiv, perm, ws, info, s, tc);
   else if (nb == 32)
@@ -1149,3 +1364,56 @@ void dlu_merge_singular(int *dst, const int *src, cudaStream_t s)
 }
 
 }  // namespace mpirg
+
+// ---- diagnostics: the binary32 trailing update alone ------------------------
+extern "C" int mpirg_ubench_gemm_f32(int n, int K, int tile, int reps, double *tflops,
+                                     double *ms_out)
+{
+  using namespace mpirg;
+  if (n <= 0 || K <= 0 || K > 128 || n % 4 || reps <= 0 || K >= n)
+    return MPIRG_ERR_INVALID_SIZE;
+  try
+  {
+    float *a = nullptr, *ut = nullptr;
+    MPIRG_CUDA_CHECK(cudaMalloc(&a, sizeof(float) * (size_t)n * n));
+    MPIRG_CUDA_CHECK(cudaMalloc(&ut, sizeof(float) * 128 * (size_t)n));
+    MPIRG_CUDA_CHECK(cudaMemset(a, 0, sizeof(float) * (size_t)n * n));
+    MPIRG_CUDA_CHECK(cudaMemset(ut, 0, sizeof(float) * 128 * (size_t)n));
+    F32Plan P;
+    f32_plan_make(P, a, n, ut, 128);
+    cudaStream_t s;
+    MPIRG_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    MPIRG_CUDA_CHECK(cudaEventCreate(&e0));
+    MPIRG_CUDA_CHECK(cudaEventCreate(&e1));
+    auto run = [&] {
+      if (tile == 128)
+        f32_gemm_t<128>(P.a128, P.u128, P, 0, K, 0, K, n, s);
+      else if (tile == 64)
+        f32_gemm_t<64>(P.a64, P.u64, P, 0, K, 0, K, n, s);
+      else
+        f32_gemm(P, 0, K, 0, K, n, s);
+    };
+    run();
+    MPIRG_CUDA_CHECK(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r)
+      run();
+    MPIRG_CUDA_CHECK(cudaEventRecord(e1, s));
+    MPIRG_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MPIRG_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    const double m = (double)(n - K);
+    *ms_out = ms / reps;
+    *tflops = 2.0 * m * m * K / (*ms_out * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    cudaFree(a);
+    cudaFree(ut);
+    return MPIRG_OK;
+  }
+  catch (const std::exception &)
+  {
+    return MPIRG_ERR_CUDA;
+  }
+}

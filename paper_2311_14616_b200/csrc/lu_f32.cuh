@@ -1,0 +1,353 @@
+// K4/K5 for binary32 factors on one GPU: U12 solve with a transposed copy of
+// U12, and a TMA-fed trailing update that can take two panel steps at once.
+//
+// Why two steps at once keeps the reference's bits (dense_lu.hpp:91-107):
+// each element a_ij takes one FMA per elimination step k, in ascending k.
+// Deferring step p's update of the far columns to step p+1 and applying
+// steps p and p+1 back to back (k = k0(p) .. k0(p+1)+nb-1, ascending) is the
+// same per-element sequence. Three things make the deferral exact:
+//   * the row moves of step p+1 are applied to the far columns AND to panel
+//     p's L columns before the deferred update, so C and L21(p) rows stay
+//     paired (a row interchange swaps whole rows, dense_lu.hpp:79-85);
+//   * the panel rows [k0(p+1), k0(p+1)+nb) of the far columns receive step
+//     p's update (the "pending" update, same FMA order) before the U12 solve
+//     of step p+1 reads them;
+//   * the update of rows below then runs K = 2nb in ascending k.
+// Halving the number of passes over the trailing matrix halves its HBM
+// traffic (8 bytes per element per pass against 2K flops), which bounds the
+// K = 64 update at large n.
+#pragma once
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace mpirg
+{
+namespace f32u
+{
+
+constexpr int MT_COLS = 32;  // columns per CTA of the U12 solve (4 warps x 8)
+
+// Row moves + (PEND: step kp's deferred update of the panel rows) + U12 =
+// L11^{-1} A12 for the columns [cb, ce); U12 is also written transposed into
+// ut[(ut_row + kk) * n + col] (row-major, contiguous along columns) so the
+// trailing update can stage it with TMA.
+template <int NB, bool PEND>
+__global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, int k0, int jb,
+                                                  int cb, int ce,
+                                                  const int2 *__restrict__ moves,
+                                                  const int *__restrict__ nmoves, int kp,
+                                                  float *__restrict__ ut, int ut_row)
+{
+  constexpr int PER = (2 * NB + 31) / 32;
+  constexpr int RL = (NB + 31) / 32;  // panel rows per lane
+  __shared__ float L[NB][NB + 1];
+  __shared__ float Lp[PEND ? NB : 1][NB + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    constexpr int PT = (NB * NB + 127) / 128;
+    float tmp[PT], tp[PEND ? PT : 1];
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int idx = threadIdx.x + u * 128;
+      const int kk = idx / NB, i = idx % NB;
+      tmp[u] = (kk < jb && i < jb) ? A[(size_t)(k0 + kk) * n + k0 + i] : 0.f;
+      if constexpr (PEND)
+        tp[u] = (kk < NB && i < jb) ? A[(size_t)(kp + kk) * n + k0 + i] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int idx = threadIdx.x + u * 128;
+      const int kk = idx / NB, i = idx % NB;
+      if (kk < NB)
+      {
+        L[i][kk] = tmp[u];
+        if constexpr (PEND)
+          Lp[i][kk] = tp[u];
+      }
+    }
+  }
+  const int nm = *nmoves;
+  const int col0 = cb + blockIdx.x * MT_COLS + warp * 8;
+  if (nm > 0)
+  {
+    int2 mv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+    {
+      const int e = lane + 32 * q;
+      mv[q] = e < nm ? moves[e] : make_int2(-1, -1);
+    }
+    float v[8][PER];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (col0 + u < ce)
+      {
+        const float *cp = A + (size_t)(col0 + u) * n;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            v[u][q] = cp[mv[q].y];
+      }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (col0 + u < ce)
+      {
+        float *cp = A + (size_t)(col0 + u) * n;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            cp[mv[q].x] = v[u][q];
+      }
+    __syncwarp();
+  }
+  __syncthreads();
+  float x[8][RL];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      x[u][h] = (col0 + u < ce && i < jb) ? A[(size_t)(col0 + u) * n + k0 + i] : 0.f;
+    }
+  if constexpr (PEND)
+  {
+    // step kp's update of the panel rows: x_i -= L(kp)[i][kk] * U(kp)[kk], kk ascending
+    float uv[8][RL];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int h = 0; h < RL; ++h)
+        uv[u][h] = (col0 + u < ce) ? A[(size_t)(col0 + u) * n + kp + lane + 32 * h] : 0.f;
+#pragma unroll 4
+    for (int kk = 0; kk < NB; ++kk)
+    {
+      const int hk = kk >> 5, lk = kk & 31;
+      float lv[RL];
+#pragma unroll
+      for (int h = 0; h < RL; ++h)
+        lv[h] = Lp[lane + 32 * h][kk];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+      {
+        float src = uv[u][0];
+#pragma unroll
+        for (int h = 1; h < RL; ++h)
+          if (hk == h)
+            src = uv[u][h];
+        const float uk = __shfl_sync(0xffffffffu, src, lk);
+#pragma unroll
+        for (int h = 0; h < RL; ++h)
+          x[u][h] = __fmaf_rn(-lv[h], uk, x[u][h]);
+      }
+    }
+  }
+#pragma unroll 1
+  for (int kk = 0; kk < jb; ++kk)
+  {
+    const int hk = kk >> 5, lk = kk & 31;
+    float lv[RL];
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      lv[h] = (i > kk && i < jb) ? L[i][kk] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+    {
+      float src = x[u][0];
+#pragma unroll
+      for (int h = 1; h < RL; ++h)
+        if (hk == h)
+          src = x[u][h];
+      const float xk = __shfl_sync(0xffffffffu, src, lk);
+#pragma unroll
+      for (int h = 0; h < RL; ++h)
+      {
+        const int i = lane + 32 * h;
+        if (i > kk && i < jb)
+          x[u][h] = __fmaf_rn(-lv[h], xk, x[u][h]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      if (col0 + u < ce && i < jb)
+        A[(size_t)(col0 + u) * n + k0 + i] = x[u][h];
+    }
+  // transposed copy through shared memory: 128-byte row segments of ut
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+      L[lane + 32 * h][warp * 8 + u] = x[u][h];
+  __syncthreads();
+  const int cbase = cb + blockIdx.x * MT_COLS;
+  for (int idx = threadIdx.x; idx < jb * MT_COLS; idx += 128)
+  {
+    const int kk = idx / MT_COLS, c = idx % MT_COLS;
+    if (cbase + c < ce)
+      ut[(size_t)(ut_row + kk) * n + cbase + c] = L[kk][c];
+  }
+}
+
+// Trailing update A[r, c] -= sum_k L[r, k] U[k, c] for rows [k0 + K, n) and
+// columns [cb, ce), k = k0 .. k0 + K - 1 ascending (K <= 128: one or two
+// panel steps). BM x BM tile per CTA of 256 threads, (BM/16)^2 accumulators
+// per thread started from A and taking one FMA per k. L21 chunks (BM rows x
+// 32 k) come from A and U12 chunks (32 k x BM columns) from the transposed
+// copy ut, both by TMA into a 3-stage ring of shared-memory buffers.
+constexpr int GKC = 32;  // k per chunk
+constexpr int GST = 3;   // ring stages
+template <int BM>
+constexpr size_t gemm_tma_smem()
+{
+  return 128 + (size_t)GST * 2 * BM * GKC * sizeof(float);
+}
+
+template <int BM>
+__global__ void __launch_bounds__(256, BM == 128 ? 2 : 3)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
+                    const __grid_constant__ CUtensorMap mapU, float *__restrict__ A, int n,
+                    int k0, int K, int ut_row, int cb, int ce)
+{
+  constexpr int TM = BM / 16;
+  constexpr uint32_t CHUNK = BM * GKC * sizeof(float);
+  extern __shared__ unsigned char gsm_raw[];
+  __shared__ __align__(8) uint64_t full[GST];
+  float *base = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(gsm_raw) + 127) &
+                                          ~uintptr_t(127));
+  float *As = base;                   // [GST][GKC][BM]
+  float *Bs = base + GST * BM * GKC;  // [GST][GKC][BM]
+  const int c0 = k0 + K;
+  const int r0 = c0 + blockIdx.x * BM;
+  const int cc0 = cb + blockIdx.y * BM;
+  const int t = threadIdx.x;
+  const int tx = t & 15, ty = t >> 4;
+  const int nch = (K + GKC - 1) / GKC;
+  if (t == 0)
+  {
+#pragma unroll
+    for (int s = 0; s < GST; ++s)
+      tc::mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int s = 0; s < GST && s < nch; ++s)
+    {
+      tc::mbar_expect_tx(&full[s], 2 * CHUNK);
+      tc::tma_load_2d(As + s * BM * GKC, &mapA, &full[s], r0, k0 + s * GKC);
+      tc::tma_load_2d(Bs + s * BM * GKC, &mapU, &full[s], cc0, ut_row + s * GKC);
+    }
+
+  float acc[TM][TM];
+#pragma unroll
+  for (int gj = 0; gj < TM / 4; ++gj)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+    {
+      const int col = cc0 + gj * 64 + ty * 4 + j;
+#pragma unroll
+      for (int gi = 0; gi < TM / 4; ++gi)
+      {
+        const int row = r0 + gi * 64 + tx * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < n && col < ce)
+          v = *reinterpret_cast<const float4 *>(A + (size_t)col * n + row);
+        acc[gi * 4 + 0][gj * 4 + j] = v.x;
+        acc[gi * 4 + 1][gj * 4 + j] = v.y;
+        acc[gi * 4 + 2][gj * 4 + j] = v.z;
+        acc[gi * 4 + 3][gj * 4 + j] = v.w;
+      }
+    }
+
+  auto step = [&](const float *ar, const float *br) {
+    float a[TM], b[TM];
+#pragma unroll
+    for (int gi = 0; gi < TM / 4; ++gi)
+    {
+      const float4 v = reinterpret_cast<const float4 *>(ar + gi * 64)[tx];
+      a[gi * 4 + 0] = v.x;
+      a[gi * 4 + 1] = v.y;
+      a[gi * 4 + 2] = v.z;
+      a[gi * 4 + 3] = v.w;
+    }
+#pragma unroll
+    for (int gj = 0; gj < TM / 4; ++gj)
+    {
+      const float4 v = reinterpret_cast<const float4 *>(br + gj * 64)[ty];
+      b[gj * 4 + 0] = v.x;
+      b[gj * 4 + 1] = v.y;
+      b[gj * 4 + 2] = v.z;
+      b[gj * 4 + 3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TM; ++j)
+        acc[i][j] = __fmaf_rn(-a[i], b[j], acc[i][j]);
+  };
+
+  for (int ch = 0; ch < nch; ++ch)
+  {
+    const int st = ch % GST;
+    tc::mbar_wait(&full[st], (ch / GST) & 1);
+    const float *as = As + st * BM * GKC;
+    const float *bs = Bs + st * BM * GKC;
+    const int kc = min(GKC, K - ch * GKC);
+    if (kc == GKC)
+    {
+#pragma unroll 8
+      for (int kk = 0; kk < GKC; ++kk)
+        step(as + kk * BM, bs + kk * BM);
+    }
+    else
+    {
+#pragma unroll 1
+      for (int kk = 0; kk < kc; ++kk)
+        step(as + kk * BM, bs + kk * BM);
+    }
+    if (ch + GST < nch)
+    {
+      __syncthreads();  // every warp is done with stage st
+      if (t == 0)
+      {
+        const int nx = ch + GST;
+        tc::mbar_expect_tx(&full[st], 2 * CHUNK);
+        tc::tma_load_2d(As + st * BM * GKC, &mapA, &full[st], r0, k0 + nx * GKC);
+        tc::tma_load_2d(Bs + st * BM * GKC, &mapU, &full[st], cc0, ut_row + nx * GKC);
+      }
+    }
+  }
+
+#pragma unroll
+  for (int gj = 0; gj < TM / 4; ++gj)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+    {
+      const int col = cc0 + gj * 64 + ty * 4 + j;
+#pragma unroll
+      for (int gi = 0; gi < TM / 4; ++gi)
+      {
+        const int row = r0 + gi * 64 + tx * 4;
+        if (row < n && col < ce)
+          *reinterpret_cast<float4 *>(A + (size_t)col * n + row) =
+              make_float4(acc[gi * 4 + 0][gj * 4 + j], acc[gi * 4 + 1][gj * 4 + j],
+                          acc[gi * 4 + 2][gj * 4 + j], acc[gi * 4 + 3][gj * 4 + j]);
+      }
+    }
+}
+
+}  // namespace f32u
+}  // namespace mpirg

@@ -85,7 +85,8 @@ def test_one_norm_matches_oracle(orc, prec, rows, cols, gpulib):
 def lu_cases():
     return [("greens", 64, 1.0), ("greens", 200, 800.0), ("greens", 257, 799.0),
             ("randn", 50, 1), ("randn", 301, 2), ("randn", 1000, 3), ("unif", 777, 4),
-            ("greens", 1500, 800.0), ("randn", 2100, 5)]
+            ("greens", 1500, 800.0), ("randn", 2100, 5), ("randn", 1088, 6),
+            ("greens", 2048, 800.0)]
 
 
 def make_case(kind, n, p):
