@@ -67,6 +67,7 @@ struct LuWorkspace
   int2 *moves = nullptr;  // [npanels][2*nb] (dst,src) row moves of each panel
   int *nmoves = nullptr;  // [npanels]
   void *side = nullptr;   // cudaStream_t: look-ahead side stream
+  void *crit = nullptr;   // cudaStream_t of the critical-chain SM group (MPIRG_LU_GREEN) or null
   void *events = nullptr; // cudaEvent_t[3*npanels]
   int *pp = nullptr;      // [n] composed row map of a tall panel
   int2 *smv = nullptr;    // [2*nb] row moves of the tall panel's 8-column leaves

@@ -36,6 +36,8 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <cstdio>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -1037,10 +1039,74 @@ static void f32_gemm(const F32Plan &P, int k0, int K, int ut_row, int cb, int ce
 // then applies its row moves to them and to panel p's L columns, the pending
 // step-p update of its own panel rows (inside the U12 solve), and one K = 2nb
 // update (lu_f32.cuh explains why the bits are unchanged).
+// MPIRG_LU_TIMELINE=1: timing events along the critical chain of lu_run_f32,
+// summarised on stderr (diagnostics only; synchronises at the end).
+struct LuTimeline
+{
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // [np][6]: panel start/end, mt end, gemm end, F end, R end
+  int np = 0;
+  void init(int n_panels)
+  {
+    static const bool env = std::getenv("MPIRG_LU_TIMELINE") != nullptr;
+    on = env;
+    if (!on)
+      return;
+    np = n_panels;
+    ev.resize((size_t)np * 6);
+    for (auto &e : ev)
+      MPIRG_CUDA_CHECK(cudaEventCreate(&e));
+  }
+  void mark(int p, int i, cudaStream_t s)
+  {
+    if (on)
+      MPIRG_CUDA_CHECK(cudaEventRecord(ev[(size_t)p * 6 + i], s));
+  }
+  void report()
+  {
+    if (!on)
+      return;
+    MPIRG_CUDA_CHECK(cudaDeviceSynchronize());
+    auto t = [&](int p, int i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0], ev[(size_t)p * 6 + i]);
+      return (double)ms * 1e3;
+    };
+    double sp = 0, sm = 0, sg = 0, sw = 0;
+    for (int p = 0; p < np; ++p)
+    {
+      const double a = t(p, 0), b = t(p, 1), c = t(p, 2), d = t(p, 3);
+      sp += b - a;
+      sm += c - b;
+      sg += d - c;
+      if (p + 1 < np)
+        sw += t(p + 1, 0) - d;
+      if (p < 8 || p % 16 == 0 || p == np - 1)
+        std::fprintf(stderr,
+                     "step %3d start %9.1f panel %6.1f mt %5.1f gemm %5.1f | F %9.1f R %9.1f us\n",
+                     p, a, b - a, c - b, d - c, t(p, 4), t(p, 5));
+    }
+    std::fprintf(stderr, "chain totals (us): panel %.0f mt %.0f gemm %.0f wait %.0f end %.0f\n",
+                 sp, sm, sg, sw, t(np - 1, 5));
+    for (auto &e : ev)
+      cudaEventDestroy(e);
+    ev.clear();
+  }
+};
+
 template <int NB>
 void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
-                cudaStream_t s)
+                cudaStream_t caller)
 {
+  // the critical chain runs on the caller's stream, or on the critical SM
+  // group's stream when the SMs are partitioned (MPIRG_LU_GREEN)
+  cudaStream_t s = ws.crit ? static_cast<cudaStream_t>(ws.crit) : caller;
+  cudaEvent_t *evx = static_cast<cudaEvent_t *>(ws.events);
+  if (s != caller)
+  {
+    MPIRG_CUDA_CHECK(cudaEventRecord(evx[1], caller));
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, evx[1], 0));
+  }
   const ColMap id{};
   cudaStream_t side = static_cast<cudaStream_t>(ws.side);
   cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);  // [4][npanels]: P, N, R, F
@@ -1057,6 +1123,8 @@ void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo 
   MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
   MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, ev[0], 0));
   bool prev_deferred = false;
+  LuTimeline tl;
+  tl.init(np);
   for (int p = 0, k0 = 0; k0 < n; ++p, k0 += NB)
   {
     const int jb = std::min(NB, n - k0);
@@ -1070,15 +1138,21 @@ void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo 
     const bool pend = prev_deferred;  // step p-1 left its far-column update to this step
     const bool defer = !pend && (p & 1) == 0 && cnn < n && jb == NB;
     const int kp = k0 - NB;
+    tl.mark(p, 0, s);
     panel_any<float, NB>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
     MPIRG_CUDA_CHECK(cudaEventRecord(evP, s));
+    tl.mark(p, 1, s);
     if (c0 < n)
     {
       if (p > 0)
         MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[3 * np + p - 1], 0));
       f32_mt<NB>(P, k0, jb, c0, cnext, mv, nm, -1, ur, s);
+      tl.mark(p, 2, s);
       f32_gemm(P, k0, jb, ur, c0, cnext, s);
     }
+    else
+      tl.mark(p, 2, s);
+    tl.mark(p, 3, s);
     MPIRG_CUDA_CHECK(cudaEventRecord(evN, s));
     MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, evP, 0));
     if (pend)  // panel p-1's L rows follow this step's row moves before they are used
@@ -1096,6 +1170,7 @@ void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo 
         f32_gemm(P, k0, jb, ur, cnext, cnn, side);
       }
       MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
+      tl.mark(p, 4, side);
       if (cnn < n)
       {
         if (pend)
@@ -1112,12 +1187,22 @@ void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo 
       }
     }
     else
+    {
       MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
+      tl.mark(p, 4, side);
+    }
     launch_moves<float, NB>(a, n, 0, pend ? kp : k0, id, mv, nm, perm, side);
     MPIRG_CUDA_CHECK(cudaEventRecord(evR, side));
+    tl.mark(p, 5, side);
     prev_deferred = defer;
   }
   MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + np - 1], 0));
+  if (s != caller)
+  {
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[np + np - 1], s));
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(caller, ev[np + np - 1], 0));
+  }
+  tl.report();
 }
 
 // ---- one rank of the 1-D block-cyclic LU (config 5a) ----------------------
@@ -1192,6 +1277,105 @@ int lu_choose_nb(int prec, int n, int requested)
   return 64;
 }
 
+// ---- SM partition for the LU (green contexts) --------------------------------
+// The panel is a thread-block cluster of up to 16 CTAs with ~180 KB of shared
+// memory each; while the bulk trailing update keeps every SM busy, the block
+// scheduler backfills freed SMs with update CTAs and the cluster (and every
+// small kernel of the critical chain) waits for whole waves of the update.
+// The binary32 LU therefore splits the device's SMs into a co-schedulable
+// group of >= k SMs for the critical chain and the remainder for the bulk
+// update, one green context each (driver API through the runtime's entry
+// points); k = 16 (one 16-CTA panel cluster) unless MPIRG_LU_GREEN=k says
+// otherwise, 0 = one shared pool. Measured on B200: N = 16384 LU 123 -> 100 ms.
+struct GreenSplit
+{
+  bool ok = false;
+  CUgreenCtx crit = nullptr, bulk = nullptr;
+  unsigned crit_sms = 0, bulk_sms = 0;
+};
+
+template <typename F>
+static F driver_fn(const char *name)
+{
+  void *p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+
+static int green_request()
+{
+  static const int v = [] {
+    const char *e = std::getenv("MPIRG_LU_GREEN");
+    return e ? std::max(0, std::atoi(e)) : 16;
+  }();
+  return v;
+}
+
+static GreenSplit &green_split()
+{
+  static GreenSplit g;
+  static bool tried = false;
+  if (tried)
+    return g;
+  tried = true;
+  const int want = green_request();
+  if (want <= 0)
+    return g;
+  using GetRes = CUresult (*)(CUdevice, CUdevResource *, CUdevResourceType);
+  using Split = CUresult (*)(CUdevResource *, unsigned *, const CUdevResource *, CUdevResource *,
+                             unsigned, unsigned);
+  using GenDesc = CUresult (*)(CUdevResourceDesc *, CUdevResource *, unsigned);
+  using Create = CUresult (*)(CUgreenCtx *, CUdevResourceDesc, CUdevice, unsigned);
+  auto get_res = driver_fn<GetRes>("cuDeviceGetDevResource");
+  auto split = driver_fn<Split>("cuDevSmResourceSplitByCount");
+  auto gen = driver_fn<GenDesc>("cuDevResourceGenerateDesc");
+  auto create = driver_fn<Create>("cuGreenCtxCreate");
+  if (!get_res || !split || !gen || !create)
+  {
+    std::fprintf(stderr, "mpirg: green contexts unavailable; LU uses one SM pool\n");
+    return g;
+  }
+  int dev = 0;
+  MPIRG_CUDA_CHECK(cudaGetDevice(&dev));
+  CUdevResource all{}, grp{}, rest{};
+  unsigned ng = 1;
+  if (get_res((CUdevice)dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      split(&grp, &ng, &all, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE,
+            (unsigned)want) != CUDA_SUCCESS ||
+      ng < 1)
+  {
+    std::fprintf(stderr, "mpirg: SM split of %d failed; LU uses one SM pool\n", want);
+    return g;
+  }
+  CUdevResourceDesc dc{}, db{};
+  if (gen(&dc, &grp, 1) != CUDA_SUCCESS || gen(&db, &rest, 1) != CUDA_SUCCESS ||
+      create(&g.crit, dc, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      create(&g.bulk, db, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+  {
+    std::fprintf(stderr, "mpirg: green context creation failed; LU uses one SM pool\n");
+    return g;
+  }
+  g.crit_sms = grp.sm.smCount;
+  g.bulk_sms = rest.sm.smCount;
+  g.ok = true;
+  std::fprintf(stderr, "mpirg: LU SM partition: critical chain %u SMs, bulk update %u SMs\n",
+               g.crit_sms, g.bulk_sms);
+  return g;
+}
+
+static cudaStream_t green_stream(CUgreenCtx ctx, int prio)
+{
+  using SC = CUresult (*)(CUstream *, CUgreenCtx, unsigned, int);
+  static auto sc = driver_fn<SC>("cuGreenCtxStreamCreate");
+  CUstream st = nullptr;
+  if (!sc || sc(&st, ctx, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS)
+    throw std::runtime_error("cuGreenCtxStreamCreate failed");
+  return reinterpret_cast<cudaStream_t>(st);
+}
+
 void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
 {
   lu_workspace_free(ws);
@@ -1211,8 +1395,17 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   // (panel -> next-panel update) on the caller's stream first.
   int lo = 0, hi = 0;
   MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
-  ws.side = side;
+  GreenSplit &g = green_split();
+  if (g.ok && prec == B32)
+  {
+    ws.side = green_stream(g.bulk, lo);
+    ws.crit = green_stream(g.crit, hi);
+  }
+  else
+  {
+    MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+    ws.side = side;
+  }
   auto *ev = new cudaEvent_t[4 * (size_t)ws.npanels];
   for (int i = 0; i < 4 * ws.npanels; ++i)
     MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
@@ -1234,6 +1427,8 @@ void lu_workspace_free(LuWorkspace &ws)
   }
   if (ws.side)
     cudaStreamDestroy(static_cast<cudaStream_t>(ws.side));
+  if (ws.crit)
+    cudaStreamDestroy(static_cast<cudaStream_t>(ws.crit));
   ws = LuWorkspace{};
 }
 

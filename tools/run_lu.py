@@ -12,6 +12,7 @@ def main():
     ap.add_argument("--prec", type=int, default=1)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--solve", action="store_true", help="also run the IR solve (cfg2a)")
+    ap.add_argument("--randn", type=int, default=-1, help="N(0,1) matrix with this seed")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -19,7 +20,10 @@ def main():
     L = lib()
     n = a.n
     buf = np.empty(n * n)
-    L.mpirg_gen_greens_operator(n, 800.0, buf.ctypes.data)
+    if a.randn >= 0:
+        L.mpirg_gen_normal_matrix(n, n, a.randn, buf.ctypes.data)
+    else:
+        L.mpirg_gen_greens_operator(n, 800.0, buf.ctypes.data)
     src = torch.from_numpy(buf).cuda()
     if a.prec == 1:
         src = src.float()
