@@ -269,9 +269,12 @@ __global__ void __launch_bounds__(NTX, 1)
   __shared__ S inbox[2][MAXCS];      // every CTA's candidate (st.async from the peers)
   // [0],[1]: exchange-step inboxes, [2]: block exchange, [3],[4]: block
   // verification flags, [5 + jj]: speculative step jj of a block
-  __shared__ __align__(8) uint64_t bars[6];
+  // [6]: a clean speculative block's pivot rows, right columns (raw)
+  __shared__ __align__(8) uint64_t bars[7];
   __shared__ BMsg<T> binbox;               // speculative block: its IB pivot rows
   __shared__ BMsg<T> bstage;               // the owner warp's staged message
+  __shared__ __align__(16) T Ubs[IB][NB];  // clean speculative block: pivot rows as of block start
+  __shared__ int spec_clean_s;
   __shared__ uint32_t vflag[2][MAXCS];     // every CTA's "speculation beaten" flag
   __shared__ int cta_beaten;
   __shared__ int piv_rank[IB], piv_lrow[IB];  // owner CTA / local row of the block's pivots
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(NTX, 1)
   const uint32_t step_bytes = (uint32_t)(CS * sizeof(S));
   if (t == 0 && multi)
   {
-    for (int i = 0; i < 6; ++i)
+    for (int i = 0; i < 7; ++i)
       mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // Arm every first phase before any peer can send: the exchange steps'
@@ -359,6 +362,8 @@ __global__ void __launch_bounds__(NTX, 1)
   int step = 0;    // exchange steps so far (inbox parity / phase bookkeeping)
   int vblk = 0;    // speculative block messages so far (bars[5] phase)
   int nverd = 0;   // verdict exchanges so far (bars[3 + parity] phases)
+  int nbx = 0;     // block-end exchanges so far (bars[2] phases)
+  int nrc = 0;     // speculative right-column messages so far (bars[6] phases)
   int skip = 0, backoff = 0;  // speculation back-off after a beaten block
 #pragma unroll 1
   for (int jb0 = 0; jb0 < jb; jb0 += IB)
@@ -378,7 +383,9 @@ __global__ void __launch_bounds__(NTX, 1)
     // (piv_rank is reset at the previous block's end / kernel start)
     // Arm the block exchange before this CTA sends any step message of the
     // block: a peer sends block data only after every CTA's last step message.
-    if (t == 0 && multi && bend < jb)
+    const bool try_spec = multi && spec_ok && skip == 0 && jb0 + IB <= jb;
+    // (a speculative block arms it at block end, only if it is beaten)
+    if (t == 0 && multi && bend < jb && !try_spec)
       mbar_expect_tx(&bars[2], (uint32_t)((bend - jb0) * rch * 16));
 
     // ---- speculative block: assume every pivot of the block is the row
@@ -393,7 +400,7 @@ __global__ void __launch_bounds__(NTX, 1)
     // in place (an earlier interchange moved them) the message says so and
     // the block takes the exchange steps directly.
     bool spec_done = false;
-    const bool try_spec = multi && spec_ok && skip == 0 && jb0 + IB <= jb;
+    bool rc_pushed = false;  // this block's right columns came with the block message
     if (!try_spec && skip > 0)
       --skip;
     if (try_spec)
@@ -402,12 +409,53 @@ __global__ void __launch_bounds__(NTX, 1)
       const int orank = (kb - k0) / R;           // CTA naturally holding [kb, kb+IB)
       const int oidx = kb - k0 - orank * R;      // = t0 + q0 * NT
       const int t0 = oidx % NT, q0 = oidx / NT;
+      if (rank == orank)
+      {
+        // the owner warp decides whether the natural rows are in place; the
+        // other warps of the owner CTA then push the pivot rows' right
+        // columns (raw, as of block start) to every CTA while it factors the
+        // block part -- the block-end exchange is then not needed
+        if (warp == t0 / 32)
+        {
+          const int li = lane - (t0 & 31);
+          bool inplace = false;
+#pragma unroll
+          for (int q = 0; q < RPT; ++q)
+            if (q == q0)
+              inplace = li >= 0 && li < IB && pos[q] == kb + li;
+          const bool cl = __popc(__ballot_sync(0xffffffffu, inplace)) == IB;
+          if (lane == 0)
+            spec_clean_s = cl ? 1 : 0;
+        }
+        __syncthreads();
+      }
+      if (rank == orank && warp != t0 / 32 && spec_clean_s && bend < jb)
+      {
+        constexpr int EPC = 16 / sizeof(T);
+        const int c_lo = jb0 + IB;
+        const int wi = warp < t0 / 32 ? warp : warp - 1;
+        const int per_row = CS * rch;
+        for (int idx = wi * 32 + lane; idx < IB * per_row; idx += (NW - 1) * 32)
+        {
+          const int jj = idx / per_row, rem = idx - jj * per_row;
+          const int dst = rem / rch, ch = rem - dst * rch;
+          T e[EPC];
+#pragma unroll
+          for (int w = 0; w < EPC; ++w)
+          {
+            const int c = c_lo + ch * EPC + w;
+            e[w] = c < jb ? P[c * R + oidx + jj] : T{};
+          }
+          st_async_v4(mapa(smem_addr(&Ubs[jj][c_lo]) + ch * 16, (uint32_t)dst),
+                      *reinterpret_cast<const uint4 *>(e),
+                      mapa(smem_addr(&bars[6]), (uint32_t)dst));
+        }
+      }
       if (rank == orank && warp == t0 / 32)
       {
         const int li = lane - (t0 & 31);  // 0..IB-1 on the block's lanes
         const bool mine = li >= 0 && li < IB;
         T rv[IB];
-        bool inplace = false;
 #pragma unroll
         for (int q = 0; q < RPT; ++q)
           if (q == q0)
@@ -415,9 +463,8 @@ __global__ void __launch_bounds__(NTX, 1)
 #pragma unroll
             for (int c = 0; c < IB; ++c)
               rv[c] = cur[q][c];
-            inplace = mine && pos[q] == kb + li;
           }
-        const bool clean = __popc(__ballot_sync(0xffffffffu, inplace)) == IB;
+        const bool clean = spec_clean_s != 0;
         if (clean)
         {
           // IB-step LU of the block's pivot rows (reference order per element)
@@ -465,6 +512,12 @@ __global__ void __launch_bounds__(NTX, 1)
         mbar_expect_tx(&bars[5], (uint32_t)sizeof(BMsg<T>));
       const bool clean = binbox.flag != 0u;
       ++vblk;
+      if (clean && bend < jb)
+      {
+        rc_pushed = true;
+        if (t == 0)
+          mbar_expect_tx(&bars[6], (uint32_t)(IB * rch * 16));
+      }
       if (clean)
       {
         bool beaten = false;
@@ -507,6 +560,19 @@ __global__ void __launch_bounds__(NTX, 1)
               for (int c = jj + 1; c < IB; ++c)
                 cur[q][c] = upd(cur[q][c], l, ub[c]);
             }
+          }
+        }
+        if (rc_pushed)
+        {
+          // take the pivot rows' right columns out of Ubs before the verdict
+          // goes out: the owner of the next block writes Ubs only after it
+          // has every CTA's verdict
+          mbar_wait(&bars[6], (uint32_t)(nrc & 1));
+          ++nrc;
+          for (int idx = t; idx < IB * (jb - bend); idx += NT)
+          {
+            const int jj = idx / (jb - bend), c = bend + idx % (jb - bend);
+            Ub[jj * NB + c] = Ubs[jj][c];
           }
         }
         PT_MARK(14);
@@ -746,8 +812,14 @@ __global__ void __launch_bounds__(NTX, 1)
       // only updated at block end), from their owners to every CTA
       const int c_lo = jb0 + IB;
       constexpr int EPC = 16 / sizeof(T);
-      if (multi)
+      if (multi && spec_done)
       {
+        // the pivot rows' right columns came with the block message
+      }
+      else if (multi)
+      {
+        if (try_spec && t == 0)  // a beaten speculative block: arm the exchange now
+          mbar_expect_tx(&bars[2], (uint32_t)((bend - jb0) * rch * 16));
         const int per_row = CS * rch;
         for (int idx = t; idx < nb_here * per_row; idx += NT)
         {
@@ -766,7 +838,8 @@ __global__ void __launch_bounds__(NTX, 1)
           st_async_v4(mapa(smem_addr(Ub + jj * NB + c_lo) + ch * 16, dst),
                       *reinterpret_cast<const uint4 *>(e), mapa(smem_addr(&bars[2]), dst));
         }
-        mbar_wait(&bars[2], (uint32_t)((jb0 / IB) & 1));
+        mbar_wait(&bars[2], (uint32_t)(nbx & 1));
+        ++nbx;
       }
       else
       {
