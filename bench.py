@@ -382,6 +382,17 @@ def run_ours(args, world, rank, local):
                 "peak_source": peak_note,
                 "peak_kind": peak_src}
     lu_ms = sum(kernel_ms[k] for k in ("panel", "moves", "trsm", "gemm"))
+    # The binary32 trailing-update kernel timed alone (no panel chain sharing
+    # the SMs): the K = 128 pass the paired LU steps launch, at this n and at
+    # the largest single-GPU LU (cfg4, n = 16384).
+    update_alone = []
+    if tf == 1:
+        for un in sorted({n if n % 4 == 0 else 0, 16384} - {0}):
+            tfl, ums = C.c_double(0.0), C.c_double(0.0)
+            if lib.mpirg_ubench_gemm_f32(un, 128, 0, 5, C.byref(tfl), C.byref(ums)) == 0:
+                update_alone.append({"n": un, "K": 128, "ms": ums.value,
+                                     "tflops": tfl.value, "peak_tflops": ffma.value,
+                                     "frac": tfl.value / ffma.value})
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -403,7 +414,7 @@ def run_ours(args, world, rank, local):
             "factor_ms": statistics.mean(fac_ms), "lu_kernels_ms": lu_ms,
             "iters": iters, "reason": reason,
             "roofline": roofline, "kernels": kernels,
-            "ffma_peak_tflops": ffma.value,
+            "ffma_peak_tflops": ffma.value, "update_kernel_alone": update_alone,
             "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(), "wall_s_timed_region": t_wall,
         }
