@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <string>
 #include <cstdio>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -1095,8 +1096,8 @@ struct LuTimeline
 };
 
 template <int NB>
-void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
-                cudaStream_t caller)
+void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                     cudaStream_t caller)
 {
   // the critical chain runs on the caller's stream, or on the critical SM
   // group's stream when the SMs are partitioned (MPIRG_LU_GREEN)
@@ -1203,6 +1204,98 @@ void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo 
     MPIRG_CUDA_CHECK(cudaStreamWaitEvent(caller, ev[np + np - 1], 0));
   }
   tl.report();
+}
+
+// The binary32 schedule issues ~6 launches per panel step across two streams;
+// on the critical chain each dependent launch costs a few microseconds of
+// launch latency. The whole schedule is therefore captured once per
+// (matrix, workspace) into a CUDA graph and replayed (MPIRG_LU_GRAPH=0 turns
+// this off; profiling and the timeline always run the streams directly).
+struct LuGraphKey
+{
+  const void *a, *ipiv, *perm, *info, *ws_moves;
+  int n;
+  cudaStream_t caller;
+  bool operator==(const LuGraphKey &o) const
+  {
+    return a == o.a && ipiv == o.ipiv && perm == o.perm && info == o.info &&
+           ws_moves == o.ws_moves && n == o.n && caller == o.caller;
+  }
+};
+struct LuGraphEntry
+{
+  LuGraphKey key;
+  cudaGraphExec_t exec;
+};
+
+static bool lu_graph_enabled()
+{
+  static const bool v = [] {
+    const char *e = std::getenv("MPIRG_LU_GRAPH");
+    return !(e && std::atoi(e) == 0) && std::getenv("MPIRG_LU_TIMELINE") == nullptr;
+  }();
+  return v;
+}
+
+static std::mutex g_lu_graph_mu;
+static std::vector<LuGraphEntry> g_lu_graphs;
+
+// Drops the cached graphs of a workspace being freed (its streams/events die).
+static void lu_graph_forget(const void *ws_moves)
+{
+  std::lock_guard<std::mutex> lk(g_lu_graph_mu);
+  for (size_t i = 0; i < g_lu_graphs.size();)
+  {
+    if (g_lu_graphs[i].key.ws_moves == ws_moves)
+    {
+      cudaGraphExecDestroy(g_lu_graphs[i].exec);
+      g_lu_graphs.erase(g_lu_graphs.begin() + i);
+    }
+    else
+      ++i;
+  }
+}
+
+template <int NB>
+void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                cudaStream_t caller)
+{
+  if (!lu_graph_enabled() || prof_on() || caller == nullptr || caller == cudaStreamLegacy ||
+      caller == cudaStreamPerThread)
+  {
+    lu_run_f32_body<NB>(a, n, ipiv, perm, ws, info, caller);
+    return;
+  }
+  const LuGraphKey key{a, ipiv, perm, info, ws.moves, n, caller};
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_lu_graph_mu);
+    for (auto &e : g_lu_graphs)
+      if (e.key == key)
+        exec = e.exec;
+  }
+  if (!exec)
+  {
+    cudaGraph_t g = nullptr;
+    MPIRG_CUDA_CHECK(cudaStreamBeginCapture(caller, cudaStreamCaptureModeThreadLocal));
+    try
+    {
+      lu_run_f32_body<NB>(a, n, ipiv, perm, ws, info, caller);
+    }
+    catch (...)
+    {
+      cudaStreamEndCapture(caller, &g);
+      if (g)
+        cudaGraphDestroy(g);
+      throw;
+    }
+    MPIRG_CUDA_CHECK(cudaStreamEndCapture(caller, &g));
+    MPIRG_CUDA_CHECK(cudaGraphInstantiate(&exec, g, 0));
+    cudaGraphDestroy(g);
+    std::lock_guard<std::mutex> lk(g_lu_graph_mu);
+    g_lu_graphs.push_back({key, exec});
+  }
+  MPIRG_CUDA_CHECK(cudaGraphLaunch(exec, caller));
 }
 
 // ---- one rank of the 1-D block-cyclic LU (config 5a) ----------------------
@@ -1414,6 +1507,8 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
 
 void lu_workspace_free(LuWorkspace &ws)
 {
+  if (ws.moves)
+    lu_graph_forget(ws.moves);
   for (void *p : {(void *)ws.moves, (void *)ws.nmoves, (void *)ws.pp, (void *)ws.smv,
                   (void *)ws.snm, ws.ut})
     if (p)
