@@ -28,6 +28,10 @@ import json
 import os
 import statistics
 import subprocess
+
+# more hardware work queues than the default 8 for the LU's concurrent
+# streams (see paper_2311_14616_b200/__init__.py); before any CUDA context
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 import threading
 import time

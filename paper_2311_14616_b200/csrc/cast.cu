@@ -118,14 +118,16 @@ __global__ void __launch_bounds__(CAST_NT) cast_norm_kernel(const From *__restri
                                                             To *__restrict__ dst, int rows,
                                                             int cols,
                                                             unsigned long long *norm_bits,
-                                                            DevInfo *info)
+                                                            DevInfo *info, int col_off)
 {
   extern __shared__ __align__(16) unsigned char cast_sm[];
   auto tile = reinterpret_cast<From(*)[CN][CCH + 1]>(cast_sm);  // [2][CN][CCH+1]
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int c0 = blockIdx.x * CN;
-  const int ncol = min(CN, cols - c0);
+  // columns [col_off, col_off + cols) of the rows x * matrix (a column chunk
+  // of a matrix that arrives in pieces keeps its storage-order indices)
+  const int c0 = col_off + blockIdx.x * CN;
+  const int ncol = min(CN, col_off + cols - c0);
   const double maxf =
       NORM_ONLY ? 0.0
                 : max_finite_of(std::is_same<To, double>::value
@@ -224,7 +226,7 @@ void demote_t(const void *src, void *dst, size_t count, DevInfo *info, cudaStrea
 
 template <typename From, typename To, bool NORM_ONLY>
 void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long long *nb,
-                 DevInfo *info, cudaStream_t s)
+                 DevInfo *info, cudaStream_t s, int col_off = 0)
 {
   if (rows <= 0 || cols <= 0)
     return;
@@ -239,7 +241,7 @@ void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long l
   }
   ProfScope ps(KC_CAST, s);
   cast_norm_kernel<From, To, NORM_ONLY><<<grid, CAST_NT, smem, s>>>(
-      static_cast<const From *>(src), static_cast<To *>(dst), rows, cols, nb, info);
+      static_cast<const From *>(src), static_cast<To *>(dst), rows, cols, nb, info, col_off);
   MPIRG_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -265,18 +267,18 @@ void launch_demote(int from, int to, const void *src, void *dst, size_t count, D
 }
 
 void launch_cast_norm(int from, int to, int rows, int cols, const void *src, void *dst,
-                      unsigned long long *nb, DevInfo *info, cudaStream_t s)
+                      unsigned long long *nb, DevInfo *info, cudaStream_t s, int col_off)
 {
   if (from == B64 && to == B64)
-    cast_norm_t<double, double, false>(rows, cols, src, dst, nb, info, s);
+    cast_norm_t<double, double, false>(rows, cols, src, dst, nb, info, s, col_off);
   else if (from == B64 && to == B32)
-    cast_norm_t<double, float, false>(rows, cols, src, dst, nb, info, s);
+    cast_norm_t<double, float, false>(rows, cols, src, dst, nb, info, s, col_off);
   else if (from == B64 && to == B16)
-    cast_norm_t<double, h16, false>(rows, cols, src, dst, nb, info, s);
+    cast_norm_t<double, h16, false>(rows, cols, src, dst, nb, info, s, col_off);
   else if (from == B32 && to == B32)
-    cast_norm_t<float, float, false>(rows, cols, src, dst, nb, info, s);
+    cast_norm_t<float, float, false>(rows, cols, src, dst, nb, info, s, col_off);
   else if (from == B32 && to == B16)
-    cast_norm_t<float, h16, false>(rows, cols, src, dst, nb, info, s);
+    cast_norm_t<float, h16, false>(rows, cols, src, dst, nb, info, s, col_off);
   else
     throw std::invalid_argument("unsupported cast");
 }

@@ -53,8 +53,11 @@ void launch_demote(int from, int to, const void *src, void *dst, size_t count, D
 // Fused refactor prologue (mp_structures.hpp:161-163): one read of the TW
 // matrix produces the TF copy, the column-sum one-norm in TW (bits of the
 // double max in *norm_bits, which must be zeroed) and the demotion flags.
+// cols columns starting at col_off of the rows x * column-major src (rows is
+// also the leading dimension); storage-order indices stay global.
 void launch_cast_norm(int from, int to, int rows, int cols, const void *src, void *dst,
-                      unsigned long long *norm_bits, DevInfo *info, cudaStream_t s);
+                      unsigned long long *norm_bits, DevInfo *info, cudaStream_t s,
+                      int col_off = 0);
 void launch_one_norm(int prec, int rows, int cols, const void *src,
                      unsigned long long *norm_bits, cudaStream_t s);
 
@@ -73,6 +76,10 @@ struct LuWorkspace
   int2 *smv = nullptr;    // [2*nb] row moves of the tall panel's 8-column leaves
   int *snm = nullptr;     // [nb/8]
   void *ut = nullptr;     // float[2*nb][n]: transposed U12 of two steps (binary32)
+  // late columns (launch_lu_late): panel snapshots, per-chunk U12 copies,
+  // per-chunk streams and events; sized for late_n
+  void *lsnap = nullptr, *utl = nullptr, *lstreams = nullptr, *levents = nullptr;
+  int late_n = 0, late_np = 0;
 };
 // Chooses the panel width for n and the factor precision (0 = auto).
 int lu_choose_nb(int prec, int n, int requested);
@@ -82,6 +89,28 @@ void lu_workspace_free(LuWorkspace &ws);
 // receives the pivot row of step k (dense_lu.hpp:79); perm (optional) the
 // accumulated permutation (row i of PA is row perm[i] of A). The first
 // exactly-zero pivot column is recorded in info->singular_col.
+// Columns that arrive while the LU runs (refactor from host memory): chunk c
+// holds columns [lo[c], hi[c]) and is present (copied and cast) once event
+// ready[c] has completed. It is brought up to date by the panel steps before
+// join[c] on its own stream -- from snapshots of those panels, so the later
+// row moves of the regular schedule cannot race with it -- and joins the
+// regular schedule at step join[c] (even, <= its first panel - 2). Chunk 0
+// must be present when the LU starts (join 0).
+struct LuLate
+{
+  static constexpr int MAXCH = 24;
+  int nch = 0;
+  int lo[MAXCH], hi[MAXCH], join[MAXCH];
+  void *ready[MAXCH];  // cudaEvent_t
+};
+// A low-priority stream on the SMs of the LU's bulk update (the whole device
+// when the SMs are not partitioned): side work that must not take the SMs of
+// the LU's critical chain.
+cudaStream_t lu_bulk_stream_create();
+// True when launch_lu_late can take (prec, lu_mode, n) (binary32 exact LU).
+bool lu_late_supported(int prec, int lu_mode, int n);
+void launch_lu_late(void *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                    cudaStream_t s, const LuLate &late);
 void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWorkspace &ws,
                DevInfo *info, cudaStream_t s);
 // perm from ipiv for callers that only hold ipiv (standalone solves).

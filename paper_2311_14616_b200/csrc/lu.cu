@@ -950,8 +950,9 @@ static int f32_mode()
 
 struct F32Plan
 {
-  CUtensorMap a128, u128, a64, u64;
+  CUtensorMap a128, u128, a64, u64;  // L21 (over ls) and U12 (over ut) boxes
   float *a = nullptr, *ut = nullptr;
+  const float *ls = nullptr;  // where the L factors are read (a, or the panel snapshots)
   int n = 0;
 };
 
@@ -970,13 +971,15 @@ static void f32_encode(CUtensorMap *map, float *base, int inner, int outer, int 
     throw std::runtime_error("cuTensorMapEncodeTiled failed for the fp32 trailing update");
 }
 
-static void f32_plan_make(F32Plan &p, float *a, int n, float *ut, int ut_rows)
+static void f32_plan_make(F32Plan &p, float *a, int n, float *ut, int ut_rows,
+                          float *ls = nullptr)
 {
   p.a = a;
   p.n = n;
   p.ut = ut;
-  f32_encode(&p.a128, a, n, n, 128);
-  f32_encode(&p.a64, a, n, n, 64);
+  p.ls = ls ? ls : a;
+  f32_encode(&p.a128, ls ? ls : a, n, n, 128);
+  f32_encode(&p.a64, ls ? ls : a, n, n, 64);
   f32_encode(&p.u128, ut, n, ut_rows, 128);
   f32_encode(&p.u64, ut, n, ut_rows, 64);
 }
@@ -991,10 +994,10 @@ static void f32_mt(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 
   const int g = (ce - cb + f32u::MT_COLS - 1) / f32u::MT_COLS;
   if (kp >= 0)
     f32u::mt2_kernel<NB, true><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, kp, P.ut,
-                                                ut_row);
+                                                ut_row, P.ls);
   else
     f32u::mt2_kernel<NB, false><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, 0, P.ut,
-                                                 ut_row);
+                                                 ut_row, P.ls);
   MPIRG_CUDA_CHECK(cudaGetLastError());
   prof_end(KC_TRSM, s);
 }
@@ -1095,9 +1098,75 @@ struct LuTimeline
   }
 };
 
+// Snapshot of panel columns [k0, k0 + jb), rows [k0, n) (a kernel, not a
+// DMA copy: the copy engines are busy with the host-to-device stream).
+__global__ void panel_snapshot_kernel(const float *__restrict__ a, float *__restrict__ dst, int n,
+                                      int k0, int jb)
+{
+  const int rows = n - k0;
+  const int r4 = (rows + 3) / 4;
+  const int tot = r4 * jb;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x)
+  {
+    const int c = i / r4, q = i - c * r4;
+    const size_t base = (size_t)(k0 + c) * n + k0;
+    const int r = 4 * q;
+    if (((k0 & 3) == 0) && r + 3 < rows)
+      *reinterpret_cast<float4 *>(dst + base + r) =
+          *reinterpret_cast<const float4 *>(a + base + r);
+    else
+      for (int e = 0; e < 4 && r + e < rows; ++e)
+        dst[base + r + e] = a[base + r + e];
+  }
+}
+
+// Late-column resources of a workspace (launch_lu_late), allocated on first use.
+struct LateRes
+{
+  float *lsnap;
+  float *utl;
+  cudaStream_t *st;
+  cudaEvent_t *ev;  // [late_np] snapshot taken, then [MAXCH] chunk caught up
+};
+
+static LateRes late_res(LuWorkspace &ws, int n, int nb)
+{
+  const int np = (n + nb - 1) / nb;
+  if (ws.late_n < n || ws.late_np < np)
+  {
+    if (ws.lsnap)
+    {
+      cudaFree(ws.lsnap);
+      cudaFree(ws.utl);
+      auto *st = static_cast<cudaStream_t *>(ws.lstreams);
+      for (int i = 0; i < LuLate::MAXCH; ++i)
+        cudaStreamDestroy(st[i]);
+      delete[] st;
+      auto *ev = static_cast<cudaEvent_t *>(ws.levents);
+      for (int i = 0; i < ws.late_np + LuLate::MAXCH; ++i)
+        cudaEventDestroy(ev[i]);
+      delete[] ev;
+    }
+    MPIRG_CUDA_CHECK(cudaMalloc(&ws.lsnap, sizeof(float) * (size_t)n * n));
+    MPIRG_CUDA_CHECK(cudaMalloc(&ws.utl, sizeof(float) * (size_t)LuLate::MAXCH * nb * n));
+    auto *st = new cudaStream_t[LuLate::MAXCH];
+    for (int i = 0; i < LuLate::MAXCH; ++i)
+      st[i] = lu_bulk_stream_create();
+    ws.lstreams = st;
+    auto *ev = new cudaEvent_t[np + LuLate::MAXCH];
+    for (int i = 0; i < np + LuLate::MAXCH; ++i)
+      MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    ws.levents = ev;
+    ws.late_n = n;
+    ws.late_np = np;
+  }
+  return {static_cast<float *>(ws.lsnap), static_cast<float *>(ws.utl),
+          static_cast<cudaStream_t *>(ws.lstreams), static_cast<cudaEvent_t *>(ws.levents)};
+}
+
 template <int NB>
 void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
-                     cudaStream_t caller)
+                     cudaStream_t caller, const LuLate *late = nullptr)
 {
   // the critical chain runs on the caller's stream, or on the critical SM
   // group's stream when the SMs are partitioned (MPIRG_LU_GREEN)
@@ -1114,6 +1183,29 @@ void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, Dev
   const int np = ws.npanels;
   F32Plan P;
   f32_plan_make(P, a, n, static_cast<float *>(ws.ut), 2 * NB);
+  // late columns: chunk c (c >= 1) is updated on its own stream from panel
+  // snapshots until step join[c]; the regular schedule's far columns end at
+  // rlim(p) = the first column of the first chunk not yet joined
+  const int nlate = late ? late->nch : 0;
+  LateRes LR{};
+  F32Plan PL[LuLate::MAXCH];
+  int last_join = 0;
+  if (nlate > 1)
+  {
+    LR = late_res(ws, n, NB);
+    for (int c = 1; c < nlate; ++c)
+    {
+      f32_plan_make(PL[c], a, n, LR.utl + (size_t)c * NB * n, NB, LR.lsnap);
+      last_join = std::max(last_join, late->join[c]);
+    }
+  }
+  auto rlim = [&](int p) {
+    int r = n;
+    for (int c = 1; c < nlate; ++c)
+      if (late->join[c] > p)
+        r = std::min(r, late->lo[c]);
+    return r;
+  };
   if (perm)
   {
     ProfScope ps(KC_VEC, s);
@@ -1137,7 +1229,8 @@ void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, Dev
     int *nm = ws.nmoves + p;
     cudaEvent_t evP = ev[p], evN = ev[np + p], evR = ev[2 * np + p], evF = ev[3 * np + p];
     const bool pend = prev_deferred;  // step p-1 left its far-column update to this step
-    const bool defer = !pend && (p & 1) == 0 && cnn < n && jb == NB;
+    const int rl = rlim(p);
+    const bool defer = !pend && (p & 1) == 0 && cnn < rl && jb == NB;
     const int kp = k0 - NB;
     tl.mark(p, 0, s);
     panel_any<float, NB>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
@@ -1156,6 +1249,36 @@ void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, Dev
     tl.mark(p, 3, s);
     MPIRG_CUDA_CHECK(cudaEventRecord(evN, s));
     MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, evP, 0));
+    if (nlate > 1 && p < last_join)
+    {
+      // snapshot of panel p (rows k0.., as it left the panel) for the late chunks
+      {
+        const int tot = ((n - k0 + 3) / 4) * jb;
+        panel_snapshot_kernel<<<std::min(148 * 2, (tot + 255) / 256), 256, 0, side>>>(
+            a, LR.lsnap, n, k0, jb);
+        MPIRG_CUDA_CHECK(cudaGetLastError());
+      }
+      MPIRG_CUDA_CHECK(cudaEventRecord(LR.ev[p], side));
+      // one stream per late chunk (they wait for different host-to-device
+      // chunks; CUDA_DEVICE_MAX_CONNECTIONS=32 keeps them off each other's
+      // hardware queues, paper_2311_14616_b200/__init__.py)
+      for (int c = 1; c < nlate; ++c)
+      {
+        if (late->join[c] <= p)
+          continue;
+        cudaStream_t ls = LR.st[c];
+        if (p == 0)
+          MPIRG_CUDA_CHECK(cudaStreamWaitEvent(ls, static_cast<cudaEvent_t>(late->ready[c]), 0));
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(ls, LR.ev[p], 0));
+        f32_mt<NB>(PL[c], k0, jb, late->lo[c], late->hi[c], mv, nm, -1, 0, ls);
+        f32_gemm(PL[c], k0, jb, 0, late->lo[c], late->hi[c], ls);
+        if (p == late->join[c] - 1)
+          MPIRG_CUDA_CHECK(cudaEventRecord(LR.ev[ws.late_np + c], ls));
+      }
+    }
+    for (int c = 1; c < nlate; ++c)
+      if (late->join[c] == p)  // chunk c joins the regular schedule at this step
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, LR.ev[ws.late_np + c], 0));
     if (pend)  // panel p-1's L rows follow this step's row moves before they are used
       launch_moves<float, NB>(a, n, kp, k0, id, mv, nm, nullptr, side);
     if (cnext < n)
@@ -1172,18 +1295,18 @@ void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, Dev
       }
       MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
       tl.mark(p, 4, side);
-      if (cnn < n)
+      if (cnn < rl)
       {
         if (pend)
         {
-          f32_mt<NB>(P, k0, jb, cnn, n, mv, nm, kp, ur, side);
-          f32_gemm(P, kp, NB + jb, 0, cnn, n, side);
+          f32_mt<NB>(P, k0, jb, cnn, rl, mv, nm, kp, ur, side);
+          f32_gemm(P, kp, NB + jb, 0, cnn, rl, side);
         }
         else
         {
-          f32_mt<NB>(P, k0, jb, cnn, n, mv, nm, -1, ur, side);
+          f32_mt<NB>(P, k0, jb, cnn, rl, mv, nm, -1, ur, side);
           if (!defer)
-            f32_gemm(P, k0, jb, ur, cnn, n, side);
+            f32_gemm(P, k0, jb, ur, cnn, rl, side);
         }
       }
     }
@@ -1469,6 +1592,18 @@ static cudaStream_t green_stream(CUgreenCtx ctx, int prio)
   return reinterpret_cast<cudaStream_t>(st);
 }
 
+cudaStream_t lu_bulk_stream_create()
+{
+  int lo = 0, hi = 0;
+  MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  GreenSplit &g = green_split();
+  if (g.ok)
+    return green_stream(g.bulk, lo);
+  cudaStream_t st;
+  MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo));
+  return st;
+}
+
 void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
 {
   lu_workspace_free(ws);
@@ -1491,12 +1626,15 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   GreenSplit &g = green_split();
   if (g.ok && prec == B32)
   {
-    ws.side = green_stream(g.bulk, lo);
+    // one level above the lowest: the side stream's look-ahead updates come
+    // before the late-column catch-up and the casts of a streamed refactor
+    ws.side = green_stream(g.bulk, std::max(hi, lo - 1));
     ws.crit = green_stream(g.crit, hi);
   }
   else
   {
-    MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+    MPIRG_CUDA_CHECK(
+        cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, std::max(hi, lo - 1)));
     ws.side = side;
   }
   auto *ev = new cudaEvent_t[4 * (size_t)ws.npanels];
@@ -1517,6 +1655,19 @@ void lu_workspace_free(LuWorkspace &ws)
   {
     auto *ev = static_cast<cudaEvent_t *>(ws.events);
     for (int i = 0; i < 4 * ws.npanels; ++i)
+      cudaEventDestroy(ev[i]);
+    delete[] ev;
+  }
+  if (ws.lsnap)
+  {
+    cudaFree(ws.lsnap);
+    cudaFree(ws.utl);
+    auto *st = static_cast<cudaStream_t *>(ws.lstreams);
+    for (int i = 0; i < LuLate::MAXCH; ++i)
+      cudaStreamDestroy(st[i]);
+    delete[] st;
+    auto *ev = static_cast<cudaEvent_t *>(ws.levents);
+    for (int i = 0; i < ws.late_np + LuLate::MAXCH; ++i)
       cudaEventDestroy(ev[i]);
     delete[] ev;
   }
@@ -1566,6 +1717,24 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
     lu_dispatch<float>(ws.nb, static_cast<float *>(a), n, ipiv, perm, ws, info, s);
   else
     lu_dispatch<h16>(ws.nb, static_cast<h16 *>(a), n, ipiv, perm, ws, info, s);
+}
+
+bool lu_late_supported(int prec, int lu_mode, int n)
+{
+  return prec == B32 && lu_mode == 0 && f32_mode() && n % 64 == 0 && n >= 1024 &&
+         n <= 32768;
+}
+
+void launch_lu_late(void *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                    cudaStream_t s, const LuLate &late)
+{
+  if (!lu_late_supported(B32, 0, n) || ws.nb != 64 || !ws.ut ||
+      reinterpret_cast<uintptr_t>(a) % 16 != 0)
+    throw std::runtime_error("launch_lu_late: unsupported configuration");
+  for (int c = 1; c < late.nch; ++c)
+    if (late.join[c] % 2 || late.join[c] * 64 + 128 > late.lo[c] || late.lo[c] % 64)
+      throw std::runtime_error("launch_lu_late: bad chunk plan");
+  lu_run_f32_body<64>(static_cast<float *>(a), n, ipiv, perm, ws, info, s, &late);
 }
 
 void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s)

@@ -31,13 +31,15 @@ constexpr int MT_COLS = 32;  // columns per CTA of the U12 solve (4 warps x 8)
 // Row moves + (PEND: step kp's deferred update of the panel rows) + U12 =
 // L11^{-1} A12 for the columns [cb, ce); U12 is also written transposed into
 // ut[(ut_row + kk) * n + col] (row-major, contiguous along columns) so the
-// trailing update can stage it with TMA.
+// trailing update can stage it with TMA. The L factors are read from Ls (the
+// matrix itself, or the snapshot of the panel taken for late columns).
 template <int NB, bool PEND>
 __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, int k0, int jb,
                                                   int cb, int ce,
                                                   const int2 *__restrict__ moves,
                                                   const int *__restrict__ nmoves, int kp,
-                                                  float *__restrict__ ut, int ut_row)
+                                                  float *__restrict__ ut, int ut_row,
+                                                  const float *__restrict__ Ls)
 {
   constexpr int PER = (2 * NB + 31) / 32;
   constexpr int RL = (NB + 31) / 32;  // panel rows per lane
@@ -52,9 +54,9 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
     {
       const int idx = threadIdx.x + u * 128;
       const int kk = idx / NB, i = idx % NB;
-      tmp[u] = (kk < jb && i < jb) ? A[(size_t)(k0 + kk) * n + k0 + i] : 0.f;
+      tmp[u] = (kk < jb && i < jb) ? Ls[(size_t)(k0 + kk) * n + k0 + i] : 0.f;
       if constexpr (PEND)
-        tp[u] = (kk < NB && i < jb) ? A[(size_t)(kp + kk) * n + k0 + i] : 0.f;
+        tp[u] = (kk < NB && i < jb) ? Ls[(size_t)(kp + kk) * n + k0 + i] : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < PT; ++u)

@@ -192,6 +192,9 @@ struct mpirg_factorization
   int underflow = 0;
   float factor_ms = 0.0f;
   cudaEvent_t ev[4] = {};
+  // refactor from host memory (refactor_streamed): copy stream + chunk events
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t cev[LuLate::MAXCH + 1] = {};
 
   size_t tw_bytes() const { return elem_size(cfg.tw); }
   size_t tf_bytes() const { return elem_size(cfg.tf); }
@@ -254,6 +257,11 @@ struct mpirg_factorization
     for (auto &e : ev)
       if (e)
         cudaEventDestroy(e);
+    for (auto &e : cev)
+      if (e)
+        cudaEventDestroy(e);
+    if (cstream)
+      cudaStreamDestroy(cstream);
     if (stream)
       cudaStreamDestroy(stream);
   }
@@ -270,6 +278,82 @@ struct mpirg_factorization
     launch_cast_norm(cfg.tw, cfg.tf, n, n, a_high, a_low, scal, info, s);
     if (do_lu)
       launch_lu(cfg.tf, cfg.lu_mode, a_low, n, ipiv, perm, luws, info, s);
+    finish_refactor(do_lu);
+  }
+
+  // refactor from a host matrix with the host-to-device copy overlapped with
+  // the factorization: the columns travel in chunks on a copy stream, each
+  // chunk is cast (and its column sums folded into ||A||_1) as it lands, and
+  // the LU starts as soon as the first chunk is in; later chunks catch up
+  // with the panels already factored and then join the schedule
+  // (launch_lu_late). Same results, bit for bit, as the copy-then-refactor
+  // path: every kernel sees the same values, only earlier.
+  static bool streamed_enabled()
+  {
+    static const bool v = [] {
+      const char *e = std::getenv("MPIRG_STREAMED_H2D");
+      return !(e && std::atoi(e) == 0);
+    }();
+    return v;
+  }
+  bool can_stream() const
+  {
+    return streamed_enabled() && lu_late_supported(cfg.tf, cfg.lu_mode, n) &&
+           lu_choose_nb(cfg.tf, n, cfg.nb) == 64;
+  }
+  void refactor_streamed(const void *host_a)
+  {
+    cudaStream_t s = stream;
+    if (!cstream)
+    {
+      cstream = lu_bulk_stream_create();
+      for (auto &e : cev)
+        MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    // chunk plan: 256 + 256 columns, then equal chunks of >= 512 columns;
+    // chunk c joins at the last even step before its first panel - 1
+    LuLate L;
+    std::vector<int> cuts{0, 256, 512};
+    const int rest = n - 512;
+    const int per = std::max(512, ((rest + (LuLate::MAXCH - 3) - 1) / (LuLate::MAXCH - 3) + 63) /
+                                      64 * 64);
+    for (int c = 512 + per; c < n; c += per)
+      cuts.push_back(c);
+    cuts.push_back(n);
+    L.nch = (int)cuts.size() - 1;
+    for (int c = 0; c < L.nch; ++c)
+    {
+      L.lo[c] = cuts[c];
+      L.hi[c] = cuts[c + 1];
+      L.join[c] = c == 0 ? 0 : std::max(0, ((cuts[c] / 64 - 2) / 2) * 2);
+      L.ready[c] = cev[c + 1];
+    }
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    reset_info(info, s);
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(scal, 0, sizeof(unsigned long long), s));
+    MPIRG_CUDA_CHECK(cudaEventRecord(cev[0], s));
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(cstream, cev[0], 0));
+    const size_t colb = (size_t)n * tw_bytes();
+    for (int c = 0; c < L.nch; ++c)
+    {
+      MPIRG_CUDA_CHECK(cudaMemcpyAsync(static_cast<char *>(a_high) + L.lo[c] * colb,
+                                       static_cast<const char *>(host_a) + L.lo[c] * colb,
+                                       (L.hi[c] - L.lo[c]) * colb, cudaMemcpyHostToDevice,
+                                       cstream));
+      launch_cast_norm(cfg.tw, cfg.tf, n, L.hi[c] - L.lo[c], a_high, a_low, scal, info, cstream,
+                       L.lo[c]);
+      MPIRG_CUDA_CHECK(cudaEventRecord(cev[c + 1], cstream));
+    }
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, cev[1], 0));
+    launch_lu_late(a_low, n, ipiv, perm, luws, info, s, L);
+    for (int c = 0; c < L.nch; ++c)
+      MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, cev[c + 1], 0));
+    finish_refactor(true);
+  }
+
+  void finish_refactor(bool do_lu)
+  {
+    cudaStream_t s = stream;
     MPIRG_CUDA_CHECK(cudaEventRecord(ev[1], s));
     MPIRG_CUDA_CHECK(cudaMemcpyAsync(h_info, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
     MPIRG_CUDA_CHECK(
@@ -611,6 +695,11 @@ int mpirg_factorization_refactor(mpirg_factorization *f, const void *a, int a_on
 {
   return guarded(err, [&] {
     MPIRG_CUDA_CHECK(cudaSetDevice(f->device));
+    if (a && !a_on_device && f->n > 0 && f->can_stream())
+    {
+      f->refactor_streamed(a);
+      return;
+    }
     if (a)
       MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->a_high, a, (size_t)f->n * f->n * f->tw_bytes(),
                                        a_on_device ? cudaMemcpyDeviceToDevice
