@@ -53,25 +53,36 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--config", default="cfg2a",
-                    choices=["cfg1", "cfg2a", "cfg2b", "cfg3", "cfg4"],
+                    choices=["cfg1", "cfg2a", "cfg2b", "cfg3", "cfg4", "cfg5a", "cfg5b"],
                     help="BASELINE config (default cfg2a = the headline workload)")
     ap.add_argument("--lu-mode", default="exact", choices=["exact", "tc"],
                     help="tc: tcgen05 trailing update for binary16 factors (cfg3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--count", type=int, default=4096,
+                    help="cfg5b: total independent systems over all ranks")
     return ap.parse_args()
 
 
-def workload(args):
-    """Seeded host inputs + reference parameters; default cfg 2a."""
+def workload(args, pinned=False):
+    """Seeded host inputs + reference parameters; default cfg 2a.
+    pinned: generate A straight into pinned host memory (cfg5a: 34 GB, one copy)."""
     from paper_2311_14616_b200 import configs
-    cfg = configs.config(args.config, args.n)
-    n = cfg["n"]
-    tag = (f"{args.config}: N={n}, <{PREC[cfg['tw']]},{PREC[cfg['tf']]},{PREC[cfg['tr']]}>, "
-           f"ce={cfg['ce']}, litmax={cfg['litmax']}"
-           + (", lu_mode=tc (tcgen05 trailing update)" if args.lu_mode == "tc" else ""))
-    cfg["workload"] = tag
+    out = None
+    if pinned:
+        import torch
+        n = args.n or configs.FULL_N[args.config]
+        out = torch.empty(n * n, dtype=torch.float64).pin_memory().numpy()
+    cfg = configs.config(args.config, args.n, out)
+    cfg["a_pinned"] = out is not None
+    cfg["workload"] = workload_tag(args, cfg)
     return cfg
+
+
+def workload_tag(args, cfg):
+    return (f"{args.config}: N={cfg['n']}, <{PREC[cfg['tw']]},{PREC[cfg['tf']]},"
+            f"{PREC[cfg['tr']]}>, ce={cfg['ce']}, litmax={cfg['litmax']}"
+            + (", lu_mode=tc (tcgen05 trailing update)" if args.lu_mode == "tc" else ""))
 
 
 def to_tw(arr64, tw):
@@ -179,24 +190,18 @@ def max_over_ranks(v, world):
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    import numpy as np
-    import oracle
-    cfg = workload(args)
-    n = cfg["n"]
-    a, b = cfg["a"], cfg["b"]
-    impl = oracle.reference()
-    kind = "reference"
-    if impl is None:
-        impl, kind = oracle.restatement(), "port"
-    af = to_tw(a, cfg["tw"]).reshape(n, n).T  # column-major storage viewed as (n, n)
-    bw = to_tw(b, cfg["tw"])
+    from paper_2311_14616_b200 import configs
+    n = args.n or configs.FULL_N[args.config]
+    if n > SAMPLE_N:  # only the N = 4096 sample is generated (reference_solve)
+        cfg = {**configs.config(args.config, SAMPLE_N), "n": n}
+        cfg["workload"] = workload_tag(args, cfg)
+    else:
+        cfg = workload(args)
+    a_w, b_w = to_tw(cfg["a"], cfg["tw"]), to_tw(cfg["b"], cfg["tw"])
     times = []
-    last = None
+    info = None
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        last = impl.ir(cfg["tw"], cfg["tf"], cfg["tr"], af, bw, on_the_fly=cfg["on_the_fly"],
-                       resid_term=cfg["resid_term"], ce=cfg["ce"], litmax=cfg["litmax"])
-        dt = time.perf_counter() - t0
+        dt, info = reference_solve(args, cfg, a_w, b_w)
         if i >= args.warmup:
             times.append(dt)
     sec = statistics.mean(times)
@@ -207,13 +212,10 @@ def run_reference(args, world, rank):
         "dtype": f"{PREC[cfg['tw']]}/{PREC[cfg['tf']]}",
         "data": "synthetic (seeded: libstdc++ mt19937_64 generators, SURVEY 8(d))",
         "config": {"workload": cfg["workload"], "n": n},
-        "cpu_baseline": {"value": sec, "unit": "s",
-                         "cores": 1 if cfg["tf"] != 2 else os.cpu_count(), "kind": kind,
-                         "sample": f"full {args.config} solve (refactor + IR) at N={n}; fp32 "
-                                   "LU single-threaded per mp_structures.hpp:166-167"},
+        "cpu_baseline": {**info, "value": sec},
         "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "reference_split_s": {"factor": last["t_factor"], "solve": last["t_solve"]},
-        "iters": len(last["rhist"]) - 1, "reason": last["reason"],
+        "reference_split_s": info["split_s"],
+        "iters": info["iters"], "reason": info["reason"],
     }
     print(json.dumps(line), flush=True)
 
@@ -241,7 +243,8 @@ def run_ours(args, world, rank, local):
     from paper_2311_14616_b200 import _lib as L
     lib = L.lib()
     torch.cuda.set_device(local)
-    wl = workload(args)
+    big = args.config == "cfg5a"
+    wl = workload(args, pinned=big)
     n = wl["n"]
     tw, tf, tr = wl["tw"], wl["tf"], wl["tr"]
     a_host, b_host = to_tw(wl["a"], tw), to_tw(wl["b"], tw)
@@ -257,6 +260,8 @@ def run_ours(args, world, rank, local):
     L.check(lib.mpirg_factorization_create(C.byref(h), n, C.byref(cfg), a_dev.data_ptr(), 1,
                                            C.byref(err)), err)
     lib.mpirg_factorization_config(h, C.byref(cfg))
+    del a_dev  # the handle holds its own copy (a_high); refactor(None) reuses it
+    torch.cuda.empty_cache()
     cap = litmax + 1
     rh, dh = (C.c_double * cap)(), (C.c_double * cap)()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -320,7 +325,8 @@ def run_ours(args, world, rank, local):
     # e2e: public API with pinned host buffers (H2D of A,b and D2H of x timed).
     e2e = None
     if not args.no_e2e:
-        a_pin = torch.from_numpy(a_host).pin_memory()
+        a_pin = (torch.from_numpy(a_host) if wl["a_pinned"] and tw == 0 else
+                 torch.from_numpy(a_host).pin_memory())
         b_pin = torch.from_numpy(b_host).pin_memory()
         x_pin = torch.empty(n, dtype=b_dev.dtype).pin_memory()
         e2e_t = []
@@ -395,8 +401,15 @@ def run_ours(args, world, rank, local):
     roofline = {"kernel": dom, "bound": roof_bound, "bound_detail": dk.get("bound"),
                 "achieved": dk.get("achieved"), "peak": dk.get("peak"), "unit": dk.get("unit"),
                 "frac": dk.get("frac"), "traffic": None,
+                "traffic_source": None,
                 "peak_source": peak_note,
                 "peak_kind": peak_src}
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path) and args.n is None and args.lu_mode == "exact":
+        tr = json.load(open(tr_path)).get(args.config, {}).get(dom)
+        if tr:
+            roofline["traffic"] = tr["bytes_per_launch"]
+            roofline["traffic_source"] = tr["capture"]
     lu_ms = sum(kernel_ms[k] for k in ("panel", "moves", "trsm", "gemm"))
     # The binary32 trailing-update kernel timed alone (no panel chain sharing
     # the SMs): the K = 128 pass the paired LU steps launch, at this n and at
@@ -410,6 +423,22 @@ def run_ours(args, world, rank, local):
                                      "tflops": tfl.value, "peak_tflops": ffma.value,
                                      "frac": tfl.value / ffma.value})
 
+    checks = None
+    if big:
+        # Size-independent properties at N = 65536 (the oracle would need hours):
+        # no interchanges (A = I - G is diagonally dominant), the reference's
+        # stopping reason, and agreement with the continuum solution of
+        # u - int g u = 1, u(t) = cos t + (1 - cos 1)/sin 1 * sin t, to the
+        # trapezoid rule's O(h^2) discretisation error.
+        ipiv = np.zeros(n, dtype=np.int32)
+        lib.mpirg_factorization_get_ipiv(h, ipiv.ctypes.data)
+        x = sol_dev.double().cpu().numpy()
+        t = np.arange(n) / (n - 1.0)
+        u = np.cos(t) + (1.0 - np.cos(1.0)) / np.sin(1.0) * np.sin(t)
+        checks = {"interchanges": int((ipiv != np.arange(n)).sum()),
+                  "max_abs_x_minus_continuum": float(np.abs(x - u).max()),
+                  "h2": (1.0 / (n - 1)) ** 2,
+                  "max_abs_x_minus_reversed": float(np.abs(x - x[::-1]).max())}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, wl, a_host, b_host)
@@ -435,31 +464,62 @@ def run_ours(args, world, rank, local):
             "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(), "wall_s_timed_region": t_wall,
         }
+        if checks:
+            line["checks"] = checks
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     lib.mpirg_factorization_destroy(h)
 
 
+SAMPLE_N = 4096  # largest N whose reference solve takes seconds, not hours
+
+
+def reference_solve(args, wl, a_host, b_host):
+    """One reference solve (oracle/_ref, else the restatement) of this workload;
+    above SAMPLE_N a bounded sample: the same operator family at N = 4096,
+    extrapolated (factor x (N/4096)^3, solve x (N/4096)^2). Returns (s, dict)."""
+    import oracle
+    n = wl["n"]
+    impl = oracle.reference()
+    kind = "reference"
+    if impl is None:
+        impl, kind = oracle.restatement(), "port"
+    scale_f = scale_s = 1.0
+    if n > SAMPLE_N:
+        from paper_2311_14616_b200 import configs
+        sw = configs.config(args.config, SAMPLE_N)
+        a_host, b_host = to_tw(sw["a"], sw["tw"]), to_tw(sw["b"], sw["tw"])
+        scale_f, scale_s = (n / SAMPLE_N) ** 3, (n / SAMPLE_N) ** 2
+        ns = SAMPLE_N
+    else:
+        ns = n
+    af = a_host.reshape(ns, ns).T
+    t0 = time.perf_counter()
+    rep = impl.ir(wl["tw"], wl["tf"], wl["tr"], af, b_host, on_the_fly=wl["on_the_fly"],
+                  resid_term=wl["resid_term"], ce=wl["ce"], litmax=wl["litmax"])
+    dt = time.perf_counter() - t0
+    if ns != n:
+        tfac, tsol = rep["t_factor"] or dt, rep["t_solve"] or 0.0
+        dt = tfac * scale_f + tsol * scale_s
+        sample = (f"one {args.config}-family solve at N={ns} (same operator and parameters) "
+                  f"by the compiled reference, factor time x(N/{ns})^3 + solve time "
+                  f"x(N/{ns})^2 extrapolated to N={n}; fp32 LU single-threaded "
+                  "(mp_structures.hpp:166-167)")
+    else:
+        sample = (f"one full {args.config} solve (refactor + IR) at N={n}; fp32 LU is "
+                  "single-threaded in the reference (mp_structures.hpp:166-167)")
+    return dt, {"unit": "s", "cores": 1 if wl["tf"] != 2 else os.cpu_count(), "kind": kind,
+                "sample": sample, "iters": len(rep["rhist"]) - 1, "reason": rep["reason"],
+                "split_s": {"factor": rep["t_factor"], "solve": rep["t_solve"]}}
+
+
 def cpu_baseline(args, wl, a_host, b_host):
     """The compiled reference (oracle/_ref) on this host: one full solve."""
-    n = wl["n"]
     try:
-        import oracle
-        impl = oracle.reference()
-        kind = "reference"
-        if impl is None:
-            impl, kind = oracle.restatement(), "port"
-        af = a_host.reshape(n, n).T
-        t0 = time.perf_counter()
-        rep = impl.ir(wl["tw"], wl["tf"], wl["tr"], af, b_host, on_the_fly=wl["on_the_fly"],
-                      resid_term=wl["resid_term"], ce=wl["ce"], litmax=wl["litmax"])
-        dt = time.perf_counter() - t0
-        return {"value": dt, "unit": "s", "cores": 1 if wl["tf"] != 2 else os.cpu_count(),
-                "kind": kind,
-                "sample": f"one full {args.config} solve (refactor + IR) at N={n}; fp32 LU is "
-                          "single-threaded in the reference (mp_structures.hpp:166-167)",
-                "iters": len(rep["rhist"]) - 1, "reason": rep["reason"]}
+        dt, d = reference_solve(args, wl, a_host, b_host)
+        d["value"] = dt
+        return d
     except Exception as e:  # pragma: no cover
         return {"value": None, "error": str(e)}
 
@@ -467,7 +527,13 @@ def cpu_baseline(args, wl, a_host, b_host):
 def main():
     args = parse()
     world, rank, local = dist_setup(args)
-    if args.impl == "reference":
+    if args.config == "cfg5b":
+        import bench_batch
+        if args.impl == "reference":
+            bench_batch.run_reference(args, world, rank)
+        else:
+            bench_batch.run_ours(args, world, rank, local)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)

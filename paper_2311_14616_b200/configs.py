@@ -48,9 +48,11 @@ def _gen():
     raise ImportError("no library with the seeded generators is built")
 
 
-def greens(n: int, alpha: float) -> np.ndarray:
-    """A = I - alpha G, column-major storage (flat, n*n)."""
-    a = np.empty(n * n, dtype=np.float64)
+def greens(n: int, alpha: float, out: np.ndarray | None = None) -> np.ndarray:
+    """A = I - alpha G, column-major storage (flat, n*n), optionally into `out`
+    (e.g. a numpy view of pinned host memory for the n = 65536 config)."""
+    a = np.empty(n * n, dtype=np.float64) if out is None else out
+    assert a.dtype == np.float64 and a.size == n * n and a.flags.c_contiguous
     _gen().mpirg_gen_greens_operator(n, alpha, a.ctypes.data)
     return a
 
@@ -61,8 +63,9 @@ def normal_vector(n: int, seed: int) -> np.ndarray:
     return v
 
 
-def config(name: str, n: int | None = None) -> dict:
-    """BASELINE.json configs[i] as the reference API call they map to."""
+def config(name: str, n: int | None = None, out: np.ndarray | None = None) -> dict:
+    """BASELINE.json configs[i] as the reference API call they map to (`out`:
+    optional host buffer for cfg5a's 34 GB matrix)."""
     n = n or FULL_N[name]
     g = _gen()
     if name == "cfg1":
@@ -88,7 +91,7 @@ def config(name: str, n: int | None = None) -> dict:
         return dict(name=name, n=n, a=a, b=b, x_true=xt, tw=B64, tf=B32, tr=B64, on_the_fly=-1,
                     resid_term=False, ce=10.0, litmax=10)
     if name == "cfg5a":
-        return dict(name=name, n=n, a=greens(n, 1.0), b=np.ones(n), tw=B64, tf=B32, tr=B64,
+        return dict(name=name, n=n, a=greens(n, 1.0, out), b=np.ones(n), tw=B64, tf=B32, tr=B64,
                     on_the_fly=-1, resid_term=False, ce=10.0, litmax=10)
     raise KeyError(name)
 

@@ -22,6 +22,7 @@ namespace
 struct Rec
 {
   int kind;
+  cudaStream_t s;  // pairs begin/end per stream (batch workers launch concurrently)
   cudaEvent_t a, b;
 };
 std::mutex g_pmu;
@@ -51,7 +52,7 @@ void prof_begin(int kind, cudaStream_t s)
   if (!g_on)
     return;
   std::lock_guard<std::mutex> lk(g_pmu);
-  Rec r{kind, take(), take()};
+  Rec r{kind, s, take(), take()};
   MPIRG_CUDA_CHECK(cudaEventRecord(r.a, s));
   g_recs.push_back(r);
   g_open.push_back((int)g_recs.size() - 1);
@@ -65,7 +66,7 @@ void prof_end(int kind, cudaStream_t s)
   for (int i = (int)g_open.size() - 1; i >= 0; --i)
   {
     Rec &r = g_recs[g_open[i]];
-    if (r.kind == kind)
+    if (r.kind == kind && r.s == s)
     {
       MPIRG_CUDA_CHECK(cudaEventRecord(r.b, s));
       g_open.erase(g_open.begin() + i);

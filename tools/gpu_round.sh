@@ -1,4 +1,5 @@
-# One GPU round: parity suite, smoke, bench lines, ncu launch list of the cfg2a bench.
+# One GPU round: parity suite, smoke, bench lines, ncu launch list of the cfg2a bench,
+# and one --set full capture of the panel and trailing-update kernels.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
@@ -10,4 +11,7 @@ timeout 900 python bench.py --config cfg4 --no-cpu-baseline --steps 3 > gpurun_o
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 MPIRG_LU_GREEN=0 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu.log 2>&1
+MPIRG_LU_GREEN=0 MPIRG_LU_GRAPH=0 timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:'lu_panel2_kernel|gemm_tma_kernel|trsv_kernel|residual_tma_kernel' -s 40 -c 6 \
+  -o gpurun_out/full_cfg2a -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log; cat gpurun_out/bench_cfg2a.json
