@@ -161,7 +161,8 @@ def run_ours(args, world, rank, local):
         if d.get("peak"):
             d["frac"] = d["achieved"] / d["peak"]
         kernels[name] = d
-    dom = max(kernels, key=lambda k: kernels[k]["ms_summed_over_streams"])
+    dom = max((k for k in kernels if "achieved" in kernels[k]),
+              key=lambda k: kernels[k]["ms_summed_over_streams"])
     dk = kernels[dom]
     roofline = {"kernel": dom, "bound": "hbm" if dk.get("bound") == "hbm" else "tensor",
                 "bound_detail": dk.get("bound"), "achieved": dk.get("achieved"),

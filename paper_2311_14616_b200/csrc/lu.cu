@@ -1002,6 +1002,62 @@ static void f32_mt(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 
   prof_end(KC_TRSM, s);
 }
 
+// The critical chain's next-column block in one fused launch (lu_f32.cuh
+// next_kernel), opt-in with MPIRG_LU_NEXT=1. Bitwise equal to the two-launch
+// form, but measured slower on B200 inside the 16-SM partition (cfg 2a LU
+// 4.56 -> 4.75 ms, profiles/r01g_next_fused_experiment.txt), so the default
+// stays mt2_kernel + gemm_tma_kernel.
+static bool next_fused()
+{
+  static const bool v = [] {
+    const char *e = std::getenv("MPIRG_LU_NEXT");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
+
+template <int NB>
+static bool f32_next(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 *mv,
+                     const int *nm, int ut_row, cudaStream_t s)
+{
+  if constexpr (NB != 64)
+    return false;
+  else
+  {
+    if (!next_fused() || P.ls != P.a || ce <= cb || ce - cb > NB)
+      return false;
+    static bool configured = false;
+    if (!configured)
+    {
+      MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::next_kernel<NB>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)f32u::next_smem<NB>()));
+      MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::next_kernel<NB>,
+                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      configured = true;
+    }
+    const int ntile = (P.n - (k0 + jb) + f32u::NX_TM - 1) / f32u::NX_TM;
+    const int cs = std::max(1, std::min(16, ntile));
+    prof_begin(KC_GEMM, s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = f32u::next_smem<NB>();
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, f32u::next_kernel<NB>, P.a, P.n, k0, jb, cb, ce,
+                                        mv, nm, P.ut, ut_row));
+    prof_end(KC_GEMM, s);
+    return true;
+  }
+}
+
 template <int BM>
 static void f32_gemm_t(const CUtensorMap &ma, const CUtensorMap &mu, const F32Plan &P, int k0,
                        int K, int ut_row, int cb, int ce, cudaStream_t s)
@@ -1240,9 +1296,14 @@ void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, Dev
     {
       if (p > 0)
         MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[3 * np + p - 1], 0));
-      f32_mt<NB>(P, k0, jb, c0, cnext, mv, nm, -1, ur, s);
-      tl.mark(p, 2, s);
-      f32_gemm(P, k0, jb, ur, c0, cnext, s);
+      if (f32_next<NB>(P, k0, jb, c0, cnext, mv, nm, ur, s))
+        tl.mark(p, 2, s);
+      else
+      {
+        f32_mt<NB>(P, k0, jb, c0, cnext, mv, nm, -1, ur, s);
+        tl.mark(p, 2, s);
+        f32_gemm(P, k0, jb, ur, c0, cnext, s);
+      }
     }
     else
       tl.mark(p, 2, s);

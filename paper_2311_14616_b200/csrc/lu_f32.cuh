@@ -351,5 +351,225 @@ __global__ void __launch_bounds__(256, BM == 128 ? 2 : 3)
     }
 }
 
+// Critical-chain step for the next panel's columns, fused into one launch:
+// panel p's row moves + U12 = L11^{-1} A12 + the K = jb update of the rows
+// below, for the column block [cb, ce) (ce - cb <= NB). Replaces mt2_kernel +
+// gemm_tma_kernel on the chain (two launches, ~30 us per step at n = 4096 on
+// the 16-SM partition) with one cluster of CS CTAs:
+//   * every CTA reads the pre-move values it needs -- the moved rows' sources
+//     and the U12 rows (a row's value after the moves is its source's value;
+//     moves permute the moved positions among themselves) -- then the cluster
+//     barrier separates every read of a pre-move value from every write;
+//   * every CTA solves U12 (one thread per column, the column in registers,
+//     k ascending, one FMA per term: mt2_kernel's bits);
+//   * CTA r updates the 64-row tiles r, r + CS, ... below: accumulators start
+//     from A (or the moved source) and take one FMA per k in ascending k, as
+//     gemm_tma_kernel does (dense_lu.hpp:91-107);
+//   * CTA 0 writes U12 back (and its transposed copy for the TMA update).
+constexpr int NX_TM = 64;  // rows per update tile (two CTAs fit an SM)
+template <int NB>
+struct NextSmem
+{
+  float Lt[NB][NX_TM];  // L21 tile, k-major
+  float Ct[NB][NX_TM + 1];  // C tile (coalesced staging of the global loads/stores)
+  float U[NB][NB + 4];  // U12 rows (k) x columns (padded: the solve reads columns)
+  float LT[NB][NB];     // L11 transposed: LT[kk][i] = l_(k0+i, k0+kk)
+  float Mv[2 * NB][NB]; // the moved rows' source values, next columns
+  int2 mv[2 * NB];
+  int um[NB];           // U12 row i <- move index, -1: not moved
+  int mvi[NX_TM];       // tile row r <- move index, -1: not moved
+};
+template <int NB>
+constexpr size_t next_smem() { return sizeof(NextSmem<NB>); }
+
+template <int NB>
+__global__ void __launch_bounds__(256, 2)
+    next_kernel(float *__restrict__ A, int n, int k0, int jb, int cb, int ce,
+                const int2 *__restrict__ moves, const int *__restrict__ nmoves,
+                float *__restrict__ ut, int ut_row)
+{
+  static_assert(NB == 64 && NX_TM == 64, "thread mapping assumes 64 x 64 blocks");
+  constexpr int PT = NB * NX_TM / 256;  // elements per thread of a 64 x 64 block
+  extern __shared__ __align__(16) unsigned char nsm[];
+  NextSmem<NB> &S = *reinterpret_cast<NextSmem<NB> *>(nsm);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int CS = (int)gridDim.x, rank = (int)blockIdx.x;  // the grid is one cluster
+  const int w = ce - cb;
+  const int r_lo = k0 + jb;
+  const int ntile = (n - r_lo + NX_TM - 1) / NX_TM;
+  const int nm = *nmoves;
+  // element u of this thread in a 64 x 64 block: column (or k) t / 64 + 4u,
+  // row t % 64 (consecutive threads read consecutive rows: coalesced)
+  const int er = t & 63, ec = t >> 6;
+
+  // ---- phase 0: pre-move reads (all loads in flight before any store)
+  {
+    float lv[PT], av[PT];
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int c = ec + 4 * u;
+      lv[u] = (c < jb && er < jb) ? A[(size_t)(k0 + c) * n + k0 + er] : 0.f;
+      av[u] = (c < w && er < jb) ? A[(size_t)(cb + c) * n + k0 + er] : 0.f;
+    }
+    for (int e = t; e < nm; e += 256)
+      S.mv[e] = moves[e];
+    if (t < NB)
+      S.um[t] = -1;
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+      S.LT[ec + 4 * u][er] = lv[u];
+    __syncthreads();
+    for (int idx = t; idx < nm * NB; idx += 256)
+    {
+      const int c = idx / nm, e = idx - c * nm;
+      S.Mv[e][c] = c < w ? A[(size_t)(cb + c) * n + S.mv[e].y] : 0.f;
+    }
+    for (int e = t; e < nm; e += 256)
+    {
+      const int d = S.mv[e].x - k0;
+      if (d >= 0 && d < jb)
+        S.um[d] = e;
+    }
+    __syncthreads();
+    const int e = S.um[er];
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int c = ec + 4 * u;
+      S.U[er][c] = (e >= 0 && c < w) ? S.Mv[e][c] : av[u];
+    }
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+
+  // first tile's L21 and C values in flight during the U12 solve
+  float pl[PT], pc[PT];
+  auto prefetch = [&](int tt) {
+    const int r0 = r_lo + tt * NX_TM;
+    const int rows = min(NX_TM, n - r0);
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int c = ec + 4 * u;
+      pl[u] = (c < jb && er < rows) ? A[(size_t)(k0 + c) * n + r0 + er] : 0.f;
+      pc[u] = (c < w && er < rows) ? A[(size_t)(cb + c) * n + r0 + er] : 0.f;
+    }
+  };
+  if (rank < ntile)
+    prefetch(rank);
+
+  // ---- phase 1: U12 = L11^{-1} A12, one thread per column (warps 0-1), the
+  // column in registers: x_i = fma(-l_ik, x_k, x_i), k ascending (the terms
+  // with k >= jb multiply zeros of LT and only touch rows >= jb, never stored)
+  if (t < NB)
+  {
+    float x[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      x[i] = S.U[i][t];
+#pragma unroll
+    for (int kk = 0; kk < NB - 1; ++kk)
+    {
+      const float xk = x[kk];
+#pragma unroll
+      for (int i4 = (kk + 1) / 4; i4 < NB / 4; ++i4)
+      {
+        const float4 l = *reinterpret_cast<const float4 *>(&S.LT[kk][4 * i4]);
+        const float lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * i4 + e > kk)
+            x[4 * i4 + e] = __fmaf_rn(-lv[e], xk, x[4 * i4 + e]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      S.U[i][t] = x[i];
+  }
+  __syncthreads();
+  if (rank == 0)
+  {
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int c = ec + 4 * u;
+      if (c < w && er < jb)
+        A[(size_t)(cb + c) * n + k0 + er] = S.U[er][c];
+    }
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int i = ec + 4 * u, c = er;  // row-major ut: consecutive threads, consecutive columns
+      if (c < w && i < jb)
+        ut[(size_t)(ut_row + i) * n + cb + c] = S.U[i][c];
+    }
+  }
+
+  // ---- phase 2: the rows below, 64-row tiles; thread: 4 rows x 4 columns
+  const int tx = t & 15, ty = t >> 4;
+  for (int tt = rank; tt < ntile; tt += CS)
+  {
+    const int r0 = r_lo + tt * NX_TM;
+    const int rows = min(NX_TM, n - r0);
+    if (t < NX_TM)
+      S.mvi[t] = -1;
+    __syncthreads();  // previous tile's readers of Lt / Ct / mvi are done
+    for (int e = t; e < nm; e += 256)
+    {
+      const int d = S.mv[e].x - r0;
+      if (d >= 0 && d < rows)
+        S.mvi[d] = e;
+    }
+    __syncthreads();
+    {
+      const int e = S.mvi[er];
+#pragma unroll
+      for (int u = 0; u < PT; ++u)
+      {
+        const int c = ec + 4 * u;
+        S.Lt[c][er] = pl[u];
+        S.Ct[c][er] = (e >= 0 && c < w) ? S.Mv[e][c] : pc[u];
+      }
+    }
+    __syncthreads();
+    if (tt + CS < ntile)
+      prefetch(tt + CS);  // next tile's loads overlap this tile's FMAs
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        acc[i][j] = S.Ct[tx * 4 + j][ty * 4 + i];
+#pragma unroll 8
+    for (int kk = 0; kk < jb; ++kk)
+    {
+      const float4 l0 = *reinterpret_cast<const float4 *>(&S.Lt[kk][ty * 4]);
+      const float4 uu = *reinterpret_cast<const float4 *>(&S.U[kk][tx * 4]);
+      const float l[4] = {l0.x, l0.y, l0.z, l0.w};
+      const float u[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[i][j] = __fmaf_rn(-l[i], u[j], acc[i][j]);
+    }
+    __syncthreads();  // every thread has read its C values
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        S.Ct[tx * 4 + j][ty * 4 + i] = acc[i][j];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PT; ++u)
+    {
+      const int c = ec + 4 * u;
+      if (c < w && er < rows)
+        A[(size_t)(cb + c) * n + r0 + er] = S.Ct[c][er];
+    }
+  }
+}
+
 }  // namespace f32u
 }  // namespace mpirg

@@ -1015,6 +1015,86 @@ int mpirg_residual(int tw, int tr, int n, const void *a, const void *x, const vo
 // systems from a shared counter; their kernels overlap on the SMs that one
 // N~1024 system leaves idle. Each system is exactly one MPFactorization +
 // ir_solve_report, so results equal the sequential ones bit for bit.
+// Device staging of a host batch (see mpirg_batch_ir_solve). Used only when
+// the host arrays are pinned (page-locked copies are truly asynchronous) and
+// the batch fits in half of the free HBM; otherwise each worker copies its own
+// system as before.
+struct BatchStage
+{
+  bool ok = false;
+  void *a = nullptr, *b = nullptr, *sol = nullptr;
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> ready;
+  int per = 16;  // systems per copy chunk
+  static bool pinned(const void *p)
+  {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess)
+    {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  }
+  void make(int count, int n, size_t tw, const void *ha, const void *hb)
+  {
+    const size_t abytes = (size_t)count * n * n * tw, vbytes = (size_t)count * n * tw;
+    size_t fr = 0, tot = 0;
+    if (!pinned(ha) || !pinned(hb) || cudaMemGetInfo(&fr, &tot) != cudaSuccess ||
+        abytes + 2 * vbytes > fr / 2)
+      return;
+    if (cudaMalloc(&a, abytes) != cudaSuccess || cudaMalloc(&b, vbytes) != cudaSuccess ||
+        cudaMalloc(&sol, vbytes) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+    {
+      cudaGetLastError();
+      release();
+      return;
+    }
+    const int nch = (count + per - 1) / per;
+    ready.assign(nch, nullptr);
+    bool good = cudaMemcpyAsync(b, hb, vbytes, cudaMemcpyHostToDevice, cs) == cudaSuccess;
+    for (int c = 0; c < nch && good; ++c)
+    {
+      const size_t lo = (size_t)c * per, hi = std::min((size_t)count, lo + per);
+      const size_t sz = (size_t)n * n * tw;
+      good = cudaEventCreateWithFlags(&ready[c], cudaEventDisableTiming) == cudaSuccess &&
+             cudaMemcpyAsync(static_cast<char *>(a) + lo * sz,
+                             static_cast<const char *>(ha) + lo * sz, (hi - lo) * sz,
+                             cudaMemcpyHostToDevice, cs) == cudaSuccess &&
+             cudaEventRecord(ready[c], cs) == cudaSuccess;
+    }
+    if (!good)
+    {
+      cudaGetLastError();
+      cudaStreamSynchronize(cs);
+      release();
+      return;
+    }
+    ok = true;
+  }
+  void release()
+  {
+    if (cs)
+      cudaStreamSynchronize(cs);
+    for (auto &e : ready)
+      if (e)
+        cudaEventDestroy(e);
+    ready.clear();
+    if (a)
+      cudaFree(a);
+    if (b)
+      cudaFree(b);
+    if (sol)
+      cudaFree(sol);
+    if (cs)
+      cudaStreamDestroy(cs);
+    a = b = sol = nullptr;
+    cs = nullptr;
+    ok = false;
+  }
+};
+
 static int batch_workers(int count, int n)
 {
   int w = n <= 1024 ? 16 : (n <= 2048 ? 8 : (n <= 4096 ? 4 : 1));
@@ -1071,13 +1151,25 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
       return st;
     }
   }
+  // Pinned host inputs: stage the batch through HBM on a copy stream in
+  // chunks of systems, issued up front. The workers take systems in index
+  // order, so the copies run ahead of the solves and overlap them, instead of
+  // one small synchronous copy per system. Solutions come back in one copy.
+  BatchStage stage;
+  if (!on_device)
+    stage.make(count, n, tw, a, b);
+  const bool staged = stage.ok;
+  const void *a_src = staged ? stage.a : a;
+  const void *b_src = staged ? stage.b : b;
+  void *sol_dst = staged ? stage.sol : sol;
+  const int src_on_device = staged ? 1 : on_device;
   auto worker = [&](int w) {
     cudaSetDevice(dev);
     mpirg_config c = *cfg;
     c.device = dev;
     mpirg_error e{};
     mpirg_factorization *f = nullptr;
-    int st = mpirg_factorization_create(&f, n, &c, nullptr, on_device, &e);
+    int st = mpirg_factorization_create(&f, n, &c, nullptr, src_on_device, &e);
     if (st != MPIRG_OK)
     {
       note(st, e);
@@ -1088,16 +1180,18 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
     cudaStreamWaitEvent(f->stream, start, 0);
     for (int sidx; (sidx = next.fetch_add(1)) < count;)
     {
-      const char *as = static_cast<const char *>(a) + (size_t)sidx * n * n * tw;
-      const char *bs = static_cast<const char *>(b) + (size_t)sidx * n * tw;
+      const char *as = static_cast<const char *>(a_src) + (size_t)sidx * n * n * tw;
+      const char *bs = static_cast<const char *>(b_src) + (size_t)sidx * n * tw;
       rhist_len[sidx] = 0;
       reason[sidx] = MPIRG_ITERATION_LIMIT;
-      st = mpirg_factorization_refactor(f, as, on_device, &e);
+      if (staged)
+        cudaStreamWaitEvent(f->stream, stage.ready[sidx / stage.per], 0);
+      st = mpirg_factorization_refactor(f, as, src_on_device, &e);
       if (st == MPIRG_OK)
       {
         mpirg_report rep{};
-        rep.sol = static_cast<char *>(sol) + (size_t)sidx * n * tw;
-        rep.sol_on_device = on_device;
+        rep.sol = static_cast<char *>(sol_dst) + (size_t)sidx * n * tw;
+        rep.sol_on_device = src_on_device;
         rep.rhist = rhist + (size_t)sidx * hist_capacity;
         rep.dhist = dhist + (size_t)sidx * hist_capacity;
         rep.hist_capacity = hist_capacity;
@@ -1119,6 +1213,13 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
   worker(0);
   for (auto &t : pool)
     t.join();
+  if (staged && cudaMemcpy(sol, stage.sol, (size_t)count * n * tw, cudaMemcpyDeviceToHost) !=
+                    cudaSuccess && first == MPIRG_OK)
+  {
+    first = MPIRG_ERR_CUDA;
+    fill_err(&first_err, MPIRG_ERR_CUDA, "batch: copy of the solutions to the host failed");
+  }
+  stage.release();
   double ms = 0.0;
   for (int w = 0; w < W; ++w)
   {

@@ -78,3 +78,47 @@ def test_batch_full_shard_size(gpulib):
     reps = mpir.batch_solve(a, np.ones((count, n)), factor="single", resid_term=False,
                             ce=10.0, litmax=10)
     assert all(r["status"] == 0 and r["reason"] == "SmallBackwardError" for r in reps)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_batch_from_host_buffers_equals_device_path(gpulib, pinned):
+    """Host inputs through the C-ABI: pinned arrays are staged through HBM in
+    chunks on a copy stream (BatchStage), pageable ones take the per-system
+    copies; both must give the device-input path's bits, singular systems
+    included."""
+    import ctypes as C
+
+    import torch
+    from paper_2311_14616_b200 import _lib as L
+    n, count = 128, 40
+    a = np.concatenate([configs.batch_system(n, i) for i in range(count)])
+    a[5 * n * n: 6 * n * n] = 0.0  # system 5 singular
+    b = np.ones(count * n)
+    cfg = L.mpirg_config(0, 1, 0, -1, 0, L.LU_EXACT, 0, 0)
+    tp = L.mpirg_term_params(1.0, 10.0, 0.5, 10)
+    cap = 11
+
+    def run(a_buf, b_buf, sol_buf, on_device):
+        rh, dh = np.zeros((count, cap)), np.zeros((count, cap))
+        rl, rs, st = (np.zeros(count, dtype=np.int32) for _ in range(3))
+        ms, err = C.c_double(0.0), L.mpirg_error()
+        gpulib.mpirg_batch_ir_solve(count, n, C.byref(cfg), a_buf.data_ptr(), b_buf.data_ptr(),
+                                    on_device, C.byref(tp), sol_buf.data_ptr(), rh.ctypes.data,
+                                    dh.ctypes.data, cap, rl.ctypes.data, rs.ctypes.data,
+                                    st.ctypes.data, C.byref(ms), C.byref(err))
+        return rh, rl, rs, st
+
+    ta, tb = torch.from_numpy(a), torch.from_numpy(b)
+    sol_d = torch.empty(count * n, dtype=torch.float64, device="cuda")
+    want = run(ta.cuda(), tb.cuda(), sol_d, 1)
+    if pinned:
+        ta, tb = ta.pin_memory(), tb.pin_memory()
+    sol_h = torch.empty(count * n, dtype=torch.float64)
+    if pinned:
+        sol_h = sol_h.pin_memory()
+    got = run(ta, tb, sol_h, 0)
+    assert list(want[3]) == list(got[3]) and want[3][5] != 0 and want[3][0] == 0
+    for w, g in zip(want[:3], got[:3]):
+        assert np.array_equal(w, g)
+    ok = np.repeat(want[3] == 0, n)
+    assert np.array_equal(sol_h.numpy()[ok].view(np.uint64), sol_d.cpu().numpy()[ok].view(np.uint64))
