@@ -195,6 +195,10 @@ struct mpirg_factorization
   // refactor from host memory (refactor_streamed): copy stream + chunk events
   cudaStream_t cstream = nullptr;
   cudaEvent_t cev[LuLate::MAXCH + 1] = {};
+  // the streamed refactor's launches as one CUDA graph, per pinned host pointer
+  const void *sg_host = nullptr;
+  int sg_seen = 0;
+  cudaGraphExec_t sg_exec = nullptr;
 
   size_t tw_bytes() const { return elem_size(cfg.tw); }
   size_t tf_bytes() const { return elem_size(cfg.tf); }
@@ -260,6 +264,8 @@ struct mpirg_factorization
     for (auto &e : cev)
       if (e)
         cudaEventDestroy(e);
+    if (sg_exec)
+      cudaGraphExecDestroy(sg_exec);
     if (cstream)
       cudaStreamDestroy(cstream);
     if (stream)
@@ -331,6 +337,76 @@ struct mpirg_factorization
     MPIRG_CUDA_CHECK(cudaEventRecord(ev[0], s));
     reset_info(info, s);
     MPIRG_CUDA_CHECK(cudaMemsetAsync(scal, 0, sizeof(unsigned long long), s));
+    // From a pinned host pointer seen before, the ~7 launches per panel step
+    // on five streams replay as one graph (the first call with a pointer runs
+    // directly: it also makes the lazily allocated late-chunk resources).
+    const bool graph = streamed_graph_enabled() && !prof_on() && host_pinned(host_a);
+    if (graph && sg_exec && sg_host == host_a)
+    {
+      MPIRG_CUDA_CHECK(cudaGraphLaunch(sg_exec, s));
+      finish_refactor(true);
+      return;
+    }
+    if (graph && sg_host != host_a)
+    {
+      if (sg_exec)
+        cudaGraphExecDestroy(sg_exec);
+      sg_exec = nullptr;
+      sg_host = host_a;
+      sg_seen = 0;
+    }
+    const bool capture = graph && sg_seen > 0;
+    if (capture)
+      MPIRG_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try
+    {
+      streamed_body(host_a, L);
+    }
+    catch (...)
+    {
+      if (capture)
+      {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(s, &g);
+        if (g)
+          cudaGraphDestroy(g);
+        sg_host = nullptr;
+      }
+      throw;
+    }
+    if (capture)
+    {
+      cudaGraph_t g = nullptr;
+      MPIRG_CUDA_CHECK(cudaStreamEndCapture(s, &g));
+      MPIRG_CUDA_CHECK(cudaGraphInstantiate(&sg_exec, g, 0));
+      cudaGraphDestroy(g);
+      MPIRG_CUDA_CHECK(cudaGraphLaunch(sg_exec, s));
+    }
+    else if (graph)
+      ++sg_seen;
+    finish_refactor(true);
+  }
+  static bool streamed_graph_enabled()
+  {
+    static const bool v = [] {
+      const char *e = std::getenv("MPIRG_STREAMED_GRAPH");
+      return !(e && std::atoi(e) == 0) && std::getenv("MPIRG_LU_TIMELINE") == nullptr;
+    }();
+    return v;
+  }
+  static bool host_pinned(const void *p)
+  {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess)
+    {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  }
+  void streamed_body(const void *host_a, const LuLate &L)
+  {
+    cudaStream_t s = stream;
     MPIRG_CUDA_CHECK(cudaEventRecord(cev[0], s));
     MPIRG_CUDA_CHECK(cudaStreamWaitEvent(cstream, cev[0], 0));
     const size_t colb = (size_t)n * tw_bytes();
@@ -348,7 +424,6 @@ struct mpirg_factorization
     launch_lu_late(a_low, n, ipiv, perm, luws, info, s, L);
     for (int c = 0; c < L.nch; ++c)
       MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, cev[c + 1], 0));
-    finish_refactor(true);
   }
 
   void finish_refactor(bool do_lu)

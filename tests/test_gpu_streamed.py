@@ -94,3 +94,29 @@ def test_streamed_refactor_reports_first_overflow(gpulib):
         f.refactor(a)
     assert str(e_host.value) == str(e_dev.value)
     assert str(e_host.value).startswith("value 9999999999999999")  # 1e39, not -2e39
+
+
+def test_streamed_refactor_graph_replay_reads_current_host_data(gpulib):
+    """From the same pinned host pointer the streamed refactor runs directly,
+    then is captured into a CUDA graph, then replayed: every call must read the
+    buffer's current contents and give the device path's bits."""
+    import torch
+    from paper_2311_14616_b200 import _lib as L
+    m = mirror()
+    n = 1536
+    mats = [greens(n, 800.0), normal_matrix(n, 11), 0.5 * greens(n, 800.0), normal_matrix(n, 12)]
+    f = m.Factorization(mats[0], working="double", factor="single", resid_term=False)
+    buf = torch.empty(n * n, dtype=torch.float64).pin_memory()
+    err = L.mpirg_error()
+    for rep in range(2):
+        for a in mats:
+            f.refactor(a)
+            want = state(f)
+            buf.numpy()[:] = np.asfortranarray(a).ravel(order="F")
+            st = lib().mpirg_factorization_refactor(f._h, C.c_void_p(buf.data_ptr()), 0,
+                                                    C.byref(err))
+            L.check(st, err)
+            got = state(f)
+            assert same_bits(got[0], want[0])
+            np.testing.assert_array_equal(got[1], want[1])
+            assert got[2] == want[2]
