@@ -84,6 +84,7 @@ struct LuWorkspace
 // Chooses the panel width for n and the factor precision (0 = auto).
 int lu_choose_nb(int prec, int n, int requested);
 void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb);
+void lu_partition_allowed(bool on);  // thread-local: next workspaces use the SM partition
 void lu_workspace_free(LuWorkspace &ws);
 // In-place LU of the n x n column-major matrix a (precision prec). ipiv[k]
 // receives the pivot row of step k (dense_lu.hpp:79); perm (optional) the

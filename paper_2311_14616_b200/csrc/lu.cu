@@ -1665,6 +1665,12 @@ cudaStream_t lu_bulk_stream_create()
   return st;
 }
 
+// Workspaces made on this thread skip the SM partition (the concurrent
+// systems of a batch each want the whole GPU for their panels, instead of
+// queueing for the 16-SM critical group; cfg 5b 0.60 -> 0.50 s).
+static thread_local bool t_partition = true;
+void lu_partition_allowed(bool on) { t_partition = on; }
+
 void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
 {
   lu_workspace_free(ws);
@@ -1685,7 +1691,7 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   int lo = 0, hi = 0;
   MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   GreenSplit &g = green_split();
-  if (g.ok && prec == B32)
+  if (g.ok && prec == B32 && t_partition)
   {
     // one level above the lowest: the side stream's look-ahead updates come
     // before the late-column catch-up and the casts of a streamed refactor

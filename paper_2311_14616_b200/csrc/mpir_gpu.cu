@@ -1244,6 +1244,11 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
     c.device = dev;
     mpirg_error e{};
     mpirg_factorization *f = nullptr;
+    struct NoPartition  // the batch's handles share the whole GPU (lu.cu)
+    {
+      NoPartition() { lu_partition_allowed(false); }
+      ~NoPartition() { lu_partition_allowed(true); }
+    } no_partition;
     int st = mpirg_factorization_create(&f, n, &c, nullptr, src_on_device, &e);
     if (st != MPIRG_OK)
     {
