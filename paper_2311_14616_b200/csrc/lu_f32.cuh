@@ -46,6 +46,14 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
   __shared__ float L[NB][NB + 1];
   __shared__ float Lp[PEND ? NB : 1][NB + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col0 = cb + blockIdx.x * MT_COLS + warp * 8;
+  // Every load that does not depend on the row moves is issued up front (the
+  // L factors, the move count, this warp's panel rows and, for PEND, step
+  // kp's U rows): on the LU's critical chain each dependent round trip costs
+  // about a microsecond. The panel rows are reloaded if rows moved.
+  float x[8][RL];
+  float uv[8][PEND ? RL : 1];
+  int nm;
   {
     constexpr int PT = (NB * NB + 127) / 128;
     float tmp[PT], tp[PEND ? PT : 1];
@@ -58,6 +66,17 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
       if constexpr (PEND)
         tp[u] = (kk < NB && i < jb) ? Ls[(size_t)(kp + kk) * n + k0 + i] : 0.f;
     }
+    nm = *nmoves;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int h = 0; h < RL; ++h)
+      {
+        const int i = lane + 32 * h;
+        x[u][h] = (col0 + u < ce && i < jb) ? A[(size_t)(col0 + u) * n + k0 + i] : 0.f;
+        if constexpr (PEND)
+          uv[u][h] = (col0 + u < ce) ? A[(size_t)(col0 + u) * n + kp + lane + 32 * h] : 0.f;
+      }
 #pragma unroll
     for (int u = 0; u < PT; ++u)
     {
@@ -71,8 +90,6 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
       }
     }
   }
-  const int nm = *nmoves;
-  const int col0 = cb + blockIdx.x * MT_COLS + warp * 8;
   if (nm > 0)
   {
     int2 mv[PER];
@@ -105,26 +122,20 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
             cp[mv[q].x] = v[u][q];
       }
     __syncwarp();
-  }
-  __syncthreads();
-  float x[8][RL];
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-#pragma unroll
-    for (int h = 0; h < RL; ++h)
-    {
-      const int i = lane + 32 * h;
-      x[u][h] = (col0 + u < ce && i < jb) ? A[(size_t)(col0 + u) * n + k0 + i] : 0.f;
-    }
-  if constexpr (PEND)
-  {
-    // step kp's update of the panel rows: x_i -= L(kp)[i][kk] * U(kp)[kk], kk ascending
-    float uv[8][RL];
+    // the panel rows after the moves (this warp's columns only)
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int h = 0; h < RL; ++h)
-        uv[u][h] = (col0 + u < ce) ? A[(size_t)(col0 + u) * n + kp + lane + 32 * h] : 0.f;
+      {
+        const int i = lane + 32 * h;
+        x[u][h] = (col0 + u < ce && i < jb) ? A[(size_t)(col0 + u) * n + k0 + i] : 0.f;
+      }
+  }
+  __syncthreads();
+  if constexpr (PEND)
+  {
+    // step kp's update of the panel rows: x_i -= L(kp)[i][kk] * U(kp)[kk], kk ascending
 #pragma unroll 4
     for (int kk = 0; kk < NB; ++kk)
     {
