@@ -62,7 +62,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--count", type=int, default=4096,
                     help="cfg5b: total independent systems over all ranks")
-    return ap.parse_args()
+    ap.add_argument("--no-also", action="store_true",
+                    help="default run only: skip the cfg4 and cfg3-tc lines attached as `also`")
+    ap.add_argument("--block-cols", type=int, default=512,
+                    help="cfg5a on N>1 GPUs: columns per block of the 1-D block-cyclic layout")
+    args = ap.parse_args()
+    args.config_given = any(a == "--config" or a.startswith("--config=") for a in sys.argv[1:])
+    return args
 
 
 def workload(args, pinned=False):
@@ -269,14 +275,23 @@ def run_ours(args, world, rank, local):
     rh, dh = (C.c_double * cap)(), (C.c_double * cap)()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
+    # one CUDA-event pair around the whole step, on the handle's own stream
+    # (torch.cuda.Event on torch's current stream would not see it)
+    hstream = torch.cuda.ExternalStream(lib.mpirg_factorization_stream(h))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
     def step(prof=False):
-        """One time-to-solution on resident data; returns (device ms, factor ms, report)."""
+        """One time-to-solution on resident data; returns (device ms between one
+        event pair around refactor + solve, factor ms, report)."""
         rep = L.mpirg_report(sol_dev.data_ptr(), 1, rh, dh, cap, 0, 0, 0, 0.0)
+        ev0.record(hstream)
         L.check(lib.mpirg_factorization_refactor(h, None, 1, C.byref(err)), err)
         fms = lib.mpirg_factorization_last_factor_ms(h)
         L.check(lib.mpirg_ir_solve(h, b_dev.data_ptr(), 1, C.byref(tp), C.byref(rep),
                                    C.byref(err)), err)
-        return fms + rep.solve_ms, fms, rep
+        ev1.record(hstream)
+        ev1.synchronize()
+        return ev0.elapsed_time(ev1), fms, rep
 
     # nvidia-smi takes ~0.1 s to start and the cfg 2a timed region lasts ~40 ms:
     # sample from the warm-up through the e2e steps (same load throughout)
@@ -404,24 +419,51 @@ def run_ours(args, world, rank, local):
         kernels[name] = d
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
-    roof_bound = "hbm" if dk.get("bound") == "hbm" else "tensor"
-    peak_note = ("MEASURED_PEAKS.json hbm_gbs" if dk.get("unit") == "GB/s" else
-                 "MEASURED_PEAKS.json bf16_tflops (tcgen05 kind::f16 rate)"
-                 if (dom == "gemm" and tc) else
+    # SURVEY 8(d) units: the LU as a whole (2N^3/3 flops over the factor time,
+    # against the FFMA peak for binary32/64 factors -- TF32/tensor cores would
+    # change the factor precision -- or the tcgen05 kind::f16 peak in tc mode),
+    # the substitution pair and the residual in algorithmic bytes over HBM.
+    fac_mean_ms = statistics.mean(fac_ms)
+    lu_unit = {"unit": "TFLOP/s", "achieved": work["total"] / (fac_mean_ms * 1e-3) / 1e12,
+               "peak": gemm_peak, "bound": "tensor" if tc else gemm_bound,
+               "work": "2N^3/3 flops over the refactor device time (cast + LU)",
+               "ms": fac_mean_ms}
+    if gemm_peak:
+        lu_unit["frac"] = lu_unit["achieved"] / gemm_peak
+    units = {"lu": lu_unit}
+    for nm in ("cast", "trsv_lower", "trsv_upper", "residual", "gemm"):
+        if nm in kernels and "frac" in kernels[nm]:
+            units[nm] = {k: kernels[nm][k] for k in ("unit", "achieved", "peak", "frac", "bound")}
+    # the contract's `roofline` object: the dominant kernel class when it has
+    # a 8(d) unit (update, cast, substitution, residual); when the latency-bound
+    # panel chain dominates (N = 4096) the LU as a unit, bound named truthfully
+    if dom in units:
+        rk, ru = dom, units[dom]
+    else:
+        rk, ru = "lu (panel chain + row moves + U12 solve + trailing update)", lu_unit
+    bound_detail = ru.get("bound")
+    roof_bound = ("hbm" if bound_detail == "hbm" else
+                  "tensor" if (tc and rk != "cast") else
+                  "latency" if (rk.startswith("lu") and dom == "panel") else bound_detail)
+    peak_note = ("MEASURED_PEAKS.json hbm_gbs" if ru.get("unit") == "GB/s" else
+                 "MEASURED_PEAKS.json bf16_tflops (tcgen05 kind::f16 rate)" if tc else
                  "fp32 FFMA microbenchmark (mpirg_ffma_peak) on this GPU; TF32/tensor cores "
                  "excluded by contract")
-    roofline = {"kernel": dom, "bound": roof_bound, "bound_detail": dk.get("bound"),
-                "achieved": dk.get("achieved"), "peak": dk.get("peak"), "unit": dk.get("unit"),
-                "frac": dk.get("frac"), "traffic": None,
+    roofline = {"kernel": rk, "bound": roof_bound, "bound_detail": bound_detail,
+                "dominant_kernel_class": dom,
+                "achieved": ru.get("achieved"), "peak": ru.get("peak"), "unit": ru.get("unit"),
+                "frac": ru.get("frac"), "traffic": None,
                 "traffic_source": None,
                 "peak_source": peak_note,
-                "peak_kind": peak_src}
+                "peak_kind": peak_src, "units": units}
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path) and args.n is None and args.lu_mode == "exact":
         trf = json.load(open(tr_path)).get(args.config, {}).get(dom)
         if trf:
             roofline["traffic"] = trf["bytes_per_launch"]
             roofline["traffic_source"] = trf["capture"]
+    if roofline["kernel"] != dom:
+        roofline["traffic_note"] = "traffic is the dominant class's (%s) per-launch DRAM bytes" % dom
     lu_ms = sum(kernel_ms[k] for k in ("panel", "moves", "trsm", "gemm"))
     # The binary32 trailing-update kernel timed alone (no panel chain sharing
     # the SMs): the K = 128 pass the paired LU steps launch, at this n and at
@@ -482,8 +524,12 @@ def run_ours(args, world, rank, local):
             line["checks"] = checks
         if cpu:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
+    else:
+        line = None
     lib.mpirg_factorization_destroy(h)
+    del hstream
+    torch.cuda.empty_cache()
+    return line
 
 
 SAMPLE_N = 4096  # largest N whose reference solve takes seconds, not hours
@@ -550,7 +596,26 @@ def main():
     elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
-        run_ours(args, world, rank, local)
+        line = run_ours(args, world, rank, local)
+        # The default invocation also times the large single-GPU configs in the
+        # same process, so their roofline fractions are driver-timed: cfg4
+        # (N = 16384, fp32 LU, pivot-heavy) and cfg3 with the tcgen05 update.
+        if (line is not None and world == 1 and not args.config_given and args.n is None
+                and args.lu_mode == "exact" and not args.no_also):
+            line["also"] = []
+            for cfg_name, mode in (("cfg4", "exact"), ("cfg3", "tc")):
+                sub = argparse.Namespace(**vars(args))
+                sub.config, sub.lu_mode, sub.no_cpu_baseline = cfg_name, mode, True
+                sub.steps, sub.warmup = min(args.steps, 3), max(3, min(args.warmup, 3))
+                try:
+                    extra = run_ours(sub, world, rank, local)
+                    for k in ("metric", "data", "clocks", "higher_is_better", "vs_baseline"):
+                        extra.pop(k, None)
+                    line["also"].append(extra)
+                except Exception as e:  # the headline line must survive
+                    line["also"].append({"config": {"workload": cfg_name}, "error": repr(e)})
+        if line is not None:
+            print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -230,7 +230,7 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
 /* ---------------------------------------------------------------------------
  * Config 5a: the 1-D block-cyclic LU across ranks.
  * One handle per rank (one process per GPU). Column block b (block_cols
- * columns, a power of two and a multiple of nb; <= 0 picks 256) lives on
+ * columns, a power of two and a multiple of nb; <= 0 picks 512) lives on
  * rank b mod nranks. Each rank holds an n x n factor buffer `a` (TF,
  * column-major, ld n; B200's 180 GB holds the full fp32 matrix of N=65536
  * per GPU) of which it owns its column blocks. Per panel p:
@@ -265,6 +265,33 @@ int mpirg_dlu_update(mpirg_dlu *h, void *a, int p, int part, int *perm, void *st
 /* Joins the side stream into `stream`, synchronises, and returns the first
  * exactly-zero pivot column seen by this rank (-1 = none). */
 int mpirg_dlu_end(mpirg_dlu *h, void *stream, int *singular_col, mpirg_error *err);
+
+/* The whole LU of this rank in one call, driven from C++ (no host round trip
+ * between a panel and its broadcast). `bcast` broadcasts `bytes` bytes of
+ * device memory at buf from rank `root`, ordered on `stream` (cudaStream_t);
+ * it is called once per panel, in panel order, on every rank, and returns 0
+ * on success. mpirg_comm_bcast (NCCL) is the product hook; tests pass a
+ * host-staged gloo broadcast. binary32 factors at nb = 64 use the single-GPU
+ * LU's TMA-fed paired-step update on the rank's columns. nranks == 1 may
+ * pass bcast = NULL. Results are bit-identical to mpirg_lu_factor. */
+typedef int (*mpirg_bcast_fn)(void *ctx, void *buf, size_t bytes, int root, void *stream);
+int mpirg_dlu_factor(mpirg_dlu *h, void *a, int *ipiv, int *perm, mpirg_bcast_fn bcast,
+                     void *ctx, void *stream, int *singular_col, mpirg_error *err);
+
+/* NCCL communicator for the hook above: one per rank, made from a 128-byte
+ * unique id created on one rank (mpirg_comm_unique_id) and handed to the
+ * others by the host side. NCCL is bound at run time (libnccl.so.2). */
+typedef struct mpirg_comm mpirg_comm;
+int mpirg_comm_unique_id(void *id128, mpirg_error *err);
+int mpirg_comm_create(mpirg_comm **out, int nranks, int rank, const void *id128, int device,
+                      mpirg_error *err);
+void mpirg_comm_destroy(mpirg_comm *c);
+int mpirg_comm_nranks(const mpirg_comm *c);
+int mpirg_comm_rank(const mpirg_comm *c);
+int mpirg_comm_version(void); /* NCCL version code, 0 when NCCL is not loadable */
+int mpirg_comm_bcast(void *comm, void *buf, size_t bytes, int root, void *stream);
+int mpirg_comm_send(mpirg_comm *c, const void *buf, size_t bytes, int peer, void *stream);
+int mpirg_comm_recv(mpirg_comm *c, void *buf, size_t bytes, int peer, void *stream);
 
 /* A handle whose LU is computed elsewhere (the distributed LU on rank 0):
  * _cast runs MPFactorization::refactor up to and including the demotion

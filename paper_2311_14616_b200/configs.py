@@ -23,29 +23,35 @@ FULL_N = {"cfg1": 4096, "cfg2a": 4096, "cfg2b": 4096, "cfg3": 8192, "cfg4": 1638
           "cfg5a": 65536, "cfg5b": 1024}
 
 
+_GEN = None
+
+
 def _gen():
-    """The seeded generators (problems.cpp), from whichever library is present."""
+    """The seeded generators (csrc/problems.cpp) from their own small host
+    library, libmpir_problems.so -- not the product library, so the bench's
+    reference arm never maps libmpir_gpu.so."""
+    global _GEN
+    if _GEN is not None:
+        return _GEN
     import os
     here = os.path.dirname(os.path.abspath(__file__))
-    for path in (os.path.join(here, "libmpir_gpu.so"),
-                 os.path.join(os.path.dirname(here), "oracle", "_ref", "libmpir_ref.so")):
-        if os.path.exists(path):
-            lib = C.CDLL(path)
-            for name, args in (("mpirg_gen_greens_operator", [C.c_int, C.c_double, C.c_void_p]),
-                               ("mpirg_gen_normal_matrix",
-                                [C.c_int, C.c_int, C.c_uint64, C.c_void_p]),
-                               ("mpirg_gen_uniform_matrix",
-                                [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double,
-                                 C.c_void_p]),
-                               ("mpirg_gen_diag_dominant",
-                                [C.c_int, C.c_uint64, C.c_double, C.c_void_p]),
-                               ("mpirg_gen_matvec_compensated_f64",
-                                [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p])):
-                fn = getattr(lib, name)
-                fn.restype = None
-                fn.argtypes = args
-            return lib
-    raise ImportError("no library with the seeded generators is built")
+    path = os.path.join(here, "libmpir_problems.so")
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing; build it with __graft_entry__.build() or "
+                          "`make -C paper_2311_14616_b200/csrc`")
+    lib = C.CDLL(path)
+    for name, args in (("mpirg_gen_greens_operator", [C.c_int, C.c_double, C.c_void_p]),
+                       ("mpirg_gen_normal_matrix", [C.c_int, C.c_int, C.c_uint64, C.c_void_p]),
+                       ("mpirg_gen_uniform_matrix",
+                        [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_void_p]),
+                       ("mpirg_gen_diag_dominant", [C.c_int, C.c_uint64, C.c_double, C.c_void_p]),
+                       ("mpirg_gen_matvec_compensated_f64",
+                        [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p])):
+        fn = getattr(lib, name)
+        fn.restype = None
+        fn.argtypes = args
+    _GEN = lib
+    return lib
 
 
 def greens(n: int, alpha: float, out: np.ndarray | None = None) -> np.ndarray:

@@ -232,12 +232,12 @@ void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long l
     return;
   const int grid = (cols + CN - 1) / CN;
   constexpr int smem = (int)(sizeof(From) * 2 * CN * (CCH + 1));
-  static bool configured = false;
-  if (!configured)
+  static DeviceOnce configured;
+  if (configured.needed())
   {
     MPIRG_CUDA_CHECK(cudaFuncSetAttribute(cast_norm_kernel<From, To, NORM_ONLY>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
+    configured.done();
   }
   ProfScope ps(KC_CAST, s);
   cast_norm_kernel<From, To, NORM_ONLY><<<grid, CAST_NT, smem, s>>>(

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -21,6 +22,29 @@ struct CudaError : std::runtime_error
   {
   }
 };
+
+// One-time setup per CUDA device (cudaFuncSetAttribute is per device/context;
+// mpirg_config.device and mpirg_dlu_create(device) let one process use
+// several). Redoing the setup from two threads at once is harmless.
+struct DeviceOnce
+{
+  std::atomic<unsigned long long> mask{0};
+  static unsigned long long bit()
+  {
+    int d = 0;
+    cudaGetDevice(&d);
+    return 1ull << (d & 63);
+  }
+  bool needed() const { return (mask.load(std::memory_order_acquire) & bit()) == 0; }
+  void done() { mask.fetch_or(bit(), std::memory_order_release); }
+};
+
+// True when a CUDA profiler/injection tool is attached to this process
+// (ncu, nsys, compute-sanitizer set CUDA_INJECTION64_PATH or
+// NV_COMPUTE_PROFILER_* / NV_SANITIZER_*): the LU then runs on plain streams
+// with no green contexts and no CUDA graphs, so every kernel of the schedule
+// is visible to the tool (prof.cu).
+bool tool_attached();
 
 // ---- profiling hooks (prof.cu) --------------------------------------------
 enum KClass
@@ -137,6 +161,11 @@ struct DluPlan
 {
   int prec = 0, n = 0, G = 1, r = 0, sh = 30;
   LuWorkspace ws;
+  // binary32 paired schedule (dlu_f32_*): tensor maps + pairing state, the
+  // communication stream and its events ([0..1] message slot free, [2] join)
+  void *f32 = nullptr;
+  void *comm = nullptr;     // cudaStream_t
+  void *cevents = nullptr;  // cudaEvent_t[3]
 };
 void dlu_alloc(DluPlan &d, int prec, int n, int nb, int G, int r, int block_cols);
 void dlu_free(DluPlan &d);
@@ -146,6 +175,21 @@ void dlu_panel(DluPlan &d, void *a, int p, int *ipiv, DevInfo *info, cudaStream_
 // 2: the remaining owned columns + left-column moves on the side stream.
 void dlu_update(DluPlan &d, void *a, int p, int part, int *perm, cudaStream_t s);
 void dlu_end(DluPlan &d, cudaStream_t s);
+// The binary32 schedule of the single-GPU LU (TMA-fed update, paired K = 2nb
+// steps, SM partition) restricted to this rank's columns. True when
+// (prec, nb, n, a) qualify; otherwise the caller uses dlu_panel/dlu_update.
+//   begin:  streams + tensor maps; `caller` is joined at dlu_f32_end
+//   crit(): the stream the owner's panel (dlu_panel) and pack must run on
+//   panel_ready(p, s): records "panel p is in this rank's buffer" on s
+//   step(p): this rank's share of step p (next panel's columns on the
+//            critical stream, the rest on the side stream)
+bool dlu_f32_supported(const DluPlan &d, const void *a);
+void dlu_f32_begin(DluPlan &d, void *a, int *perm, cudaStream_t caller);
+cudaStream_t dlu_f32_crit(DluPlan &d);
+cudaStream_t dlu_f32_comm(DluPlan &d);
+void dlu_f32_panel_ready(DluPlan &d, int p, cudaStream_t s);
+void dlu_f32_step(DluPlan &d, int p, int *perm, bool own_panel);
+void dlu_f32_end(DluPlan &d, cudaStream_t caller);
 void dlu_merge_singular(int *dst, const int *src, cudaStream_t s);
 
 // ---- K6: triangular solves ------------------------------------------------

@@ -587,26 +587,26 @@ __global__ void min_into_kernel(int *dst, const int *src) { *dst = min(*dst, *sr
 template <typename T, int NB, int RPT, int NTX>
 void configure_panel()
 {
-  static bool done = false;
-  if (done)
+  static DeviceOnce done;
+  if (!done.needed())
     return;
   auto k = panel2::lu_panel2_kernel<T, NB, RPT, NTX>;
   MPIRG_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   MPIRG_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)panel2::panel_dyn_smem<T, NB, RPT, NTX>()));
-  done = true;
+  done.done();
 }
 
 template <typename T, int NB>
 void configure_gemm()
 {
-  static bool done = false;
-  if (done)
+  static DeviceOnce done;
+  if (!done.needed())
     return;
   MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_kernel<T, NB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)gemm_smem_bytes<T, NB>()));
-  done = true;
+  done.done();
 }
 
 // Speculative pivoting in the panel (lu_panel.cuh); MPIRG_PANEL_SPEC=0 turns
@@ -748,13 +748,13 @@ void launch_mt(T *a, int n, int k0, int jb, int cb, int ce, ColMap map, const in
 template <int NB, int BM, int BN>
 void launch_gemm_v4_t(float *a, int n, int k0, int jb, int cb, int ce, ColMap map, cudaStream_t s)
 {
-  static bool configured = false;
-  if (!configured)
+  static DeviceOnce configured;
+  if (configured.needed())
   {
     MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_v4_kernel<NB, BM, BN>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)gemm_v4_smem<NB, BM, BN>()));
-    configured = true;
+    configured.done();
   }
   const int c0 = k0 + jb;
   const dim3 grid((n - c0 + BM - 1) / BM, (ce - cb + BN - 1) / BN);
@@ -1026,15 +1026,15 @@ static bool f32_next(const F32Plan &P, int k0, int jb, int cb, int ce, const int
   {
     if (!next_fused() || P.ls != P.a || ce <= cb || ce - cb > NB)
       return false;
-    static bool configured = false;
-    if (!configured)
+    static DeviceOnce configured;
+    if (configured.needed())
     {
       MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::next_kernel<NB>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)f32u::next_smem<NB>()));
       MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::next_kernel<NB>,
                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      configured = true;
+      configured.done();
     }
     const int ntile = (P.n - (k0 + jb) + f32u::NX_TM - 1) / f32u::NX_TM;
     const int cs = std::max(1, std::min(16, ntile));
@@ -1062,13 +1062,13 @@ template <int BM>
 static void f32_gemm_t(const CUtensorMap &ma, const CUtensorMap &mu, const F32Plan &P, int k0,
                        int K, int ut_row, int cb, int ce, cudaStream_t s)
 {
-  static bool configured = false;
-  if (!configured)
+  static DeviceOnce configured;
+  if (configured.needed())
   {
     MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::gemm_tma_kernel<BM>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)f32u::gemm_tma_smem<BM>()));
-    configured = true;
+    configured.done();
   }
   const int c0 = k0 + K;
   const dim3 grid((P.n - c0 + BM - 1) / BM, (ce - cb + BM - 1) / BM);
@@ -1416,7 +1416,8 @@ static bool lu_graph_enabled()
 {
   static const bool v = [] {
     const char *e = std::getenv("MPIRG_LU_GRAPH");
-    return !(e && std::atoi(e) == 0) && std::getenv("MPIRG_LU_TIMELINE") == nullptr;
+    return !(e && std::atoi(e) == 0) && std::getenv("MPIRG_LU_TIMELINE") == nullptr &&
+           !tool_attached();
   }();
   return v;
 }
@@ -1532,6 +1533,105 @@ void dlu_update_t(DluPlan &d, T *a, int p, int part, int *perm, cudaStream_t s)
   }
 }
 
+// ---- one rank of the 1-D block-cyclic LU, binary32 paired schedule -------------
+// lu_run_f32_body with ownership: every column range of the single-GPU step
+// is cut into this rank's contiguous runs (whole distribution blocks, or the
+// parts of them inside the range); with G = 1 there is one run per range and
+// the launches are exactly the single-GPU ones. Panel p reaches the rank's
+// buffer by dlu_panel (owner) or by the caller's broadcast + unpack; its L
+// columns are kept by every rank until the paired update of step p+1 has read
+// them, so step p+1's row moves are applied to every rank's copy.
+struct DluF32State
+{
+  F32Plan P;
+  float *a = nullptr;
+  bool prev_deferred = false;
+  cudaStream_t s = nullptr;
+};
+
+template <typename F>
+static void for_owned_runs(const DluPlan &d, int lo, int hi, F &&f)
+{
+  if (lo >= hi)
+    return;
+  if (d.G == 1)
+  {
+    f(lo, hi);
+    return;
+  }
+  const int B = 1 << d.sh;
+  for (int b = lo >> d.sh; b * B < hi; ++b)
+  {
+    if (b % d.G != d.r)
+      continue;
+    const int gb = std::max(lo, b * B), ge = std::min(hi, (b + 1) * B);
+    if (gb < ge)
+      f(gb, ge);
+  }
+}
+
+template <int NB>
+static void dlu_f32_step_t(DluPlan &d, int p, int *perm, bool own_panel)
+{
+  auto &st = *static_cast<DluF32State *>(d.f32);
+  LuWorkspace &ws = d.ws;
+  const F32Plan &P = st.P;
+  float *a = st.a;
+  const ColMap map{d.G, d.r, d.sh};
+  const ColMap id{};
+  const int n = d.n, np = ws.npanels;
+  cudaStream_t s = st.s, side = static_cast<cudaStream_t>(ws.side);
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);  // [4][np]: P, N, R, F
+  const int k0 = p * NB, jb = std::min(NB, n - k0), c0 = k0 + jb;
+  const int cnext = std::min(n, c0 + NB), cnn = std::min(n, cnext + NB);
+  const int ur = (p & 1) * NB;
+  const int2 *mv = ws.moves + (size_t)p * 2 * NB;
+  const int *nm = ws.nmoves + p;
+  cudaEvent_t evP = ev[p], evR = ev[2 * np + p], evF = ev[3 * np + p];
+  const bool pend = st.prev_deferred;
+  const bool defer = !pend && (p & 1) == 0 && cnn < n && jb == NB;
+  const int kp = k0 - NB;
+  auto mine = [&](int c) { return d.G == 1 || ((c >> d.sh) % d.G) == d.r; };
+  // critical chain: the next panel's columns, when this rank factors them
+  if (c0 < n && mine(c0))
+  {
+    if (!own_panel)
+      MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, evP, 0));
+    if (p > 0)
+      MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[3 * np + p - 1], 0));
+    f32_mt<NB>(P, k0, jb, c0, cnext, mv, nm, -1, ur, s);
+    f32_gemm(P, k0, jb, ur, c0, cnext, s);
+  }
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, evP, 0));
+  if (pend)  // this rank's copy of panel p-1's L rows follows step p's row moves
+    launch_moves<float, NB>(a, n, kp, k0, id, mv, nm, nullptr, side);
+  auto update = [&](int gb, int ge, bool do_gemm) {
+    if (pend)
+    {
+      f32_mt<NB>(P, k0, jb, gb, ge, mv, nm, kp, ur, side);
+      f32_gemm(P, kp, NB + jb, 0, gb, ge, side);
+    }
+    else
+    {
+      f32_mt<NB>(P, k0, jb, gb, ge, mv, nm, -1, ur, side);
+      if (do_gemm)
+        f32_gemm(P, k0, jb, ur, gb, ge, side);
+    }
+  };
+  if (cnext < n)
+  {
+    if (mine(cnext))
+      update(cnext, cnn, true);
+    MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
+    for_owned_runs(d, cnn, n, [&](int gb, int ge) { update(gb, ge, !defer); });
+  }
+  else
+    MPIRG_CUDA_CHECK(cudaEventRecord(evF, side));
+  launch_moves<float, NB>(a, n, 0, map.lcount(pend ? kp : k0), map, mv, nm, perm, side);
+  MPIRG_CUDA_CHECK(cudaEventRecord(evR, side));
+  st.prev_deferred = defer;
+}
+
 template <typename T, int NB>
 void dlu_panel_t(DluPlan &d, T *a, int p, int *ipiv, DevInfo *info, cudaStream_t s)
 {
@@ -1598,7 +1698,9 @@ static GreenSplit &green_split()
   if (tried)
     return g;
   tried = true;
-  const int want = green_request();
+  // no SM partition under a profiler/sanitizer: the tools cannot follow
+  // launches into green contexts (ncu died at the first LU launch)
+  const int want = tool_attached() ? 0 : green_request();
   if (want <= 0)
     return g;
   using GetRes = CUresult (*)(CUdevice, CUdevResource *, CUdevResourceType);
@@ -1690,8 +1792,9 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   // (panel -> next-panel update) on the caller's stream first.
   int lo = 0, hi = 0;
   MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // small systems finish their panels faster than the partition pays for
   GreenSplit &g = green_split();
-  if (g.ok && prec == B32 && t_partition)
+  if (g.ok && prec == B32 && t_partition && n >= 2048)
   {
     // one level above the lowest: the side stream's look-ahead updates come
     // before the late-column catch-up and the casts of a streamed refactor
@@ -1824,7 +1927,23 @@ void dlu_alloc(DluPlan &d, int prec, int n, int nb, int G, int r, int block_cols
   lu_workspace_alloc(d.ws, prec, n, nb);
 }
 
-void dlu_free(DluPlan &d) { lu_workspace_free(d.ws); }
+void dlu_free(DluPlan &d)
+{
+  lu_workspace_free(d.ws);
+  delete static_cast<DluF32State *>(d.f32);
+  d.f32 = nullptr;
+  if (d.cevents)
+  {
+    auto *ce = static_cast<cudaEvent_t *>(d.cevents);
+    for (int i = 0; i < 3; ++i)
+      cudaEventDestroy(ce[i]);
+    delete[] ce;
+    d.cevents = nullptr;
+  }
+  if (d.comm)
+    cudaStreamDestroy(static_cast<cudaStream_t>(d.comm));
+  d.comm = nullptr;
+}
 
 void dlu_begin(DluPlan &d, int *perm, cudaStream_t s)
 {
@@ -1881,6 +2000,83 @@ void dlu_end(DluPlan &d, cudaStream_t s)
   // every REST event that was recorded (part 2 calls) is before the last one
   MPIRG_CUDA_CHECK(cudaEventRecord(ev[np + np - 1], static_cast<cudaStream_t>(d.ws.side)));
   MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[np + np - 1], 0));
+}
+
+bool dlu_f32_supported(const DluPlan &d, const void *a)
+{
+  return d.prec == B32 && d.ws.nb == 64 && f32_mode() && d.ws.ut && d.n % 4 == 0 &&
+         reinterpret_cast<uintptr_t>(a) % 16 == 0;
+}
+
+void dlu_f32_begin(DluPlan &d, void *a, int *perm, cudaStream_t caller)
+{
+  LuWorkspace &ws = d.ws;
+  if (!d.f32)
+    d.f32 = new DluF32State;
+  auto &st = *static_cast<DluF32State *>(d.f32);
+  st.a = static_cast<float *>(a);
+  st.prev_deferred = false;
+  st.s = ws.crit ? static_cast<cudaStream_t>(ws.crit) : caller;
+  f32_plan_make(st.P, st.a, d.n, static_cast<float *>(ws.ut), 2 * ws.nb);
+  if (!d.comm)
+  {
+    int lo = 0, hi = 0;
+    MPIRG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    cudaStream_t c;
+    MPIRG_CUDA_CHECK(cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, hi));
+    d.comm = c;
+    auto *ce = new cudaEvent_t[3];
+    for (int i = 0; i < 3; ++i)
+      MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&ce[i], cudaEventDisableTiming));
+    d.cevents = ce;
+  }
+  cudaEvent_t *ce = static_cast<cudaEvent_t *>(d.cevents);
+  cudaStream_t comm = static_cast<cudaStream_t>(d.comm), side = static_cast<cudaStream_t>(ws.side);
+  // every stream starts after the caller's earlier work (the cast)
+  if (perm)
+  {
+    iota_kernel<<<(d.n + 255) / 256, 256, 0, caller>>>(perm, d.n);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  }
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(ws.nmoves, 0, sizeof(int) * ws.npanels, caller));
+  MPIRG_CUDA_CHECK(cudaEventRecord(ce[2], caller));
+  for (cudaStream_t t : {st.s, side, comm})
+    if (t != caller)
+      MPIRG_CUDA_CHECK(cudaStreamWaitEvent(t, ce[2], 0));
+  // both message slots start free
+  MPIRG_CUDA_CHECK(cudaEventRecord(ce[0], comm));
+  MPIRG_CUDA_CHECK(cudaEventRecord(ce[1], comm));
+}
+
+cudaStream_t dlu_f32_crit(DluPlan &d) { return static_cast<DluF32State *>(d.f32)->s; }
+cudaStream_t dlu_f32_comm(DluPlan &d) { return static_cast<cudaStream_t>(d.comm); }
+
+void dlu_f32_panel_ready(DluPlan &d, int p, cudaStream_t s)
+{
+  MPIRG_CUDA_CHECK(cudaEventRecord(static_cast<cudaEvent_t *>(d.ws.events)[p], s));
+}
+
+void dlu_f32_step(DluPlan &d, int p, int *perm, bool own_panel)
+{
+  dlu_f32_step_t<64>(d, p, perm, own_panel);
+}
+
+void dlu_f32_end(DluPlan &d, cudaStream_t caller)
+{
+  auto &st = *static_cast<DluF32State *>(d.f32);
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(d.ws.events);
+  cudaEvent_t *ce = static_cast<cudaEvent_t *>(d.cevents);
+  const int np = d.ws.npanels;
+  // the side stream's last record (evR of the last step) covers every step's
+  // bulk work; the critical and communication streams join through ce[2]
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(caller, ev[2 * np + np - 1], 0));
+  if (st.s != caller)
+  {
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[np + np - 1], st.s));
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(caller, ev[np + np - 1], 0));
+  }
+  MPIRG_CUDA_CHECK(cudaEventRecord(ce[2], static_cast<cudaStream_t>(d.comm)));
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(caller, ce[2], 0));
 }
 
 void dlu_merge_singular(int *dst, const int *src, cudaStream_t s)

@@ -154,13 +154,13 @@ void launch_gemm_tc(const TcPlan &p, int k0, int cb, int ce, cudaStream_t s)
   const int n = p.n, c0 = k0 + TK;
   if (ce <= cb || c0 >= n)
     return;
-  static bool configured = false;
-  if (!configured)
+  static DeviceOnce configured;
+  if (configured.needed())
   {
     MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_tc_kernel,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)TC_SMEM));
-    configured = true;
+    configured.done();
   }
   // C tiles: the matrix viewed with ce columns, so the store never touches
   // columns outside this update's range (another stream may own them).

@@ -210,6 +210,13 @@ struct mpirg_factorization
     const int need = 2 + 3 * (litmax + 1);
     if (need <= scal_cap)
       return;
+    // the streamed-refactor graph has the old scal pointer baked into its
+    // cast kernels (||A||_1 slot): drop it, the next refactor re-captures
+    if (sg_exec)
+      cudaGraphExecDestroy(sg_exec);
+    sg_exec = nullptr;
+    sg_host = nullptr;
+    sg_seen = 0;
     if (scal)
       cudaFree(scal);
     if (h_scal)
@@ -390,7 +397,8 @@ struct mpirg_factorization
   {
     static const bool v = [] {
       const char *e = std::getenv("MPIRG_STREAMED_GRAPH");
-      return !(e && std::atoi(e) == 0) && std::getenv("MPIRG_LU_TIMELINE") == nullptr;
+      return !(e && std::atoi(e) == 0) && std::getenv("MPIRG_LU_TIMELINE") == nullptr &&
+             !tool_attached();
     }();
     return v;
   }
@@ -1275,7 +1283,7 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
         rep.rhist = rhist + (size_t)sidx * hist_capacity;
         rep.dhist = dhist + (size_t)sidx * hist_capacity;
         rep.hist_capacity = hist_capacity;
-        st = mpirg_ir_solve(f, bs, on_device, tp, &rep, &e);
+        st = mpirg_ir_solve(f, bs, src_on_device, tp, &rep, &e);
         rhist_len[sidx] = rep.rhist_len;
         reason[sidx] = rep.reason;
       }
@@ -1293,11 +1301,31 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
   worker(0);
   for (auto &t : pool)
     t.join();
-  if (staged && cudaMemcpy(sol, stage.sol, (size_t)count * n * tw, cudaMemcpyDeviceToHost) !=
-                    cudaSuccess && first == MPIRG_OK)
+  if (staged)
   {
-    first = MPIRG_ERR_CUDA;
-    fill_err(&first_err, MPIRG_ERR_CUDA, "batch: copy of the solutions to the host failed");
+    // runs of solved systems only: a failed system's slice of `sol` stays
+    // untouched, as on the non-staged path
+    bool copied = true;
+    for (int lo = 0; lo < count && copied;)
+    {
+      if (status[lo] != MPIRG_OK)
+      {
+        ++lo;
+        continue;
+      }
+      int hi = lo;
+      while (hi < count && status[hi] == MPIRG_OK)
+        ++hi;
+      const size_t off = (size_t)lo * n * tw;
+      copied = cudaMemcpy(static_cast<char *>(sol) + off, static_cast<char *>(stage.sol) + off,
+                          (size_t)(hi - lo) * n * tw, cudaMemcpyDeviceToHost) == cudaSuccess;
+      lo = hi;
+    }
+    if (!copied && first == MPIRG_OK)
+    {
+      first = MPIRG_ERR_CUDA;
+      fill_err(&first_err, MPIRG_ERR_CUDA, "batch: copy of the solutions to the host failed");
+    }
   }
   stage.release();
   double ms = 0.0;
@@ -1368,6 +1396,8 @@ struct mpirg_dlu
   int nb = 0, np = 0, block_cols = 0;
   DevInfo *info = nullptr;
   int *hdr = nullptr;  // scratch for a received header
+  void *msg[2] = {nullptr, nullptr};  // step messages of mpirg_dlu_factor (two slots)
+  cudaEvent_t packed[2] = {nullptr, nullptr};
 };
 
 namespace
@@ -1409,7 +1439,7 @@ int mpirg_dlu_create(mpirg_dlu **out, int prec, int n, int nb, int nranks, int r
     if (device >= 0)
       MPIRG_CUDA_CHECK(cudaSetDevice(device));
     const int b = lu_choose_nb(prec, n, nb);
-    int bc = block_cols > 0 ? block_cols : std::max(256, b);
+    int bc = block_cols > 0 ? block_cols : std::max(512, b);  // north_star: block 512
     if ((bc & (bc - 1)) != 0 || bc % b != 0)
       throw ApiError{MPIRG_ERR_INVALID_PARAM,
                      "block_cols must be a power of two and a multiple of nb"};
@@ -1446,6 +1476,13 @@ void mpirg_dlu_destroy(mpirg_dlu *h)
     cudaFree(h->info);
   if (h->hdr)
     cudaFree(h->hdr);
+  for (int i = 0; i < 2; ++i)
+  {
+    if (h->msg[i])
+      cudaFree(h->msg[i]);
+    if (h->packed[i])
+      cudaEventDestroy(h->packed[i]);
+  }
   delete h;
 }
 
@@ -1480,29 +1517,53 @@ int mpirg_dlu_panel(mpirg_dlu *h, void *a, int p, int *ipiv, void *stream, mpirg
 }
 
 // Step message: [nmoves, singular_col | ipiv[jb] | moves[2 nb] | panel rows k0..n-1 x jb].
+static void pack_on(mpirg_dlu *h, const void *a, int p, const int *ipiv, void *msg,
+                    cudaStream_t s)
+{
+  const MsgLayout L = msg_layout(h, p);
+  const int n = h->plan.n, k0 = p * h->nb, jb = std::min(h->nb, n - k0);
+  const size_t es = elem_size(h->plan.prec);
+  char *m = static_cast<char *>(msg);
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(m, h->plan.ws.nmoves + p, sizeof(int),
+                                   cudaMemcpyDeviceToDevice, s));
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + 4, &h->info->singular_col, sizeof(int),
+                                   cudaMemcpyDeviceToDevice, s));
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + L.ipiv, ipiv + k0, sizeof(int) * jb,
+                                   cudaMemcpyDeviceToDevice, s));
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + L.moves, h->plan.ws.moves + (size_t)p * 2 * h->nb,
+                                   sizeof(int2) * 2 * h->nb, cudaMemcpyDeviceToDevice, s));
+  MPIRG_CUDA_CHECK(cudaMemcpy2DAsync(m + L.panel, (n - k0) * es,
+                                     static_cast<const char *>(a) + ((size_t)k0 * n + k0) * es,
+                                     (size_t)n * es, (n - k0) * es, jb,
+                                     cudaMemcpyDeviceToDevice, s));
+}
+
+static void unpack_on(mpirg_dlu *h, void *a, int p, int *ipiv, const void *msg, cudaStream_t s)
+{
+  const MsgLayout L = msg_layout(h, p);
+  const int n = h->plan.n, k0 = p * h->nb, jb = std::min(h->nb, n - k0);
+  const size_t es = elem_size(h->plan.prec);
+  const char *m = static_cast<const char *>(msg);
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->plan.ws.nmoves + p, m, sizeof(int),
+                                   cudaMemcpyDeviceToDevice, s));
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->hdr, m + 4, sizeof(int), cudaMemcpyDeviceToDevice, s));
+  dlu_merge_singular(&h->info->singular_col, h->hdr, s);
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(ipiv + k0, m + L.ipiv, sizeof(int) * jb,
+                                   cudaMemcpyDeviceToDevice, s));
+  MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->plan.ws.moves + (size_t)p * 2 * h->nb, m + L.moves,
+                                   sizeof(int2) * 2 * h->nb, cudaMemcpyDeviceToDevice, s));
+  MPIRG_CUDA_CHECK(cudaMemcpy2DAsync(static_cast<char *>(a) + ((size_t)k0 * n + k0) * es,
+                                     (size_t)n * es, m + L.panel, (n - k0) * es,
+                                     (n - k0) * es, jb, cudaMemcpyDeviceToDevice, s));
+}
+
 int mpirg_dlu_pack(mpirg_dlu *h, const void *a, int p, const int *ipiv, void *msg,
                    void *stream, mpirg_error *err)
 {
   return guarded(err, [&] {
     check_step(h, p);
     MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
-    auto s = static_cast<cudaStream_t>(stream);
-    const MsgLayout L = msg_layout(h, p);
-    const int n = h->plan.n, k0 = p * h->nb, jb = std::min(h->nb, n - k0);
-    const size_t es = elem_size(h->plan.prec);
-    char *m = static_cast<char *>(msg);
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m, h->plan.ws.nmoves + p, sizeof(int),
-                                     cudaMemcpyDeviceToDevice, s));
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + 4, &h->info->singular_col, sizeof(int),
-                                     cudaMemcpyDeviceToDevice, s));
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + L.ipiv, ipiv + k0, sizeof(int) * jb,
-                                     cudaMemcpyDeviceToDevice, s));
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(m + L.moves, h->plan.ws.moves + (size_t)p * 2 * h->nb,
-                                     sizeof(int2) * 2 * h->nb, cudaMemcpyDeviceToDevice, s));
-    MPIRG_CUDA_CHECK(cudaMemcpy2DAsync(m + L.panel, (n - k0) * es,
-                                       static_cast<const char *>(a) + ((size_t)k0 * n + k0) * es,
-                                       (size_t)n * es, (n - k0) * es, jb,
-                                       cudaMemcpyDeviceToDevice, s));
+    pack_on(h, a, p, ipiv, msg, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1512,22 +1573,111 @@ int mpirg_dlu_unpack(mpirg_dlu *h, void *a, int p, int *ipiv, const void *msg, v
   return guarded(err, [&] {
     check_step(h, p);
     MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
-    auto s = static_cast<cudaStream_t>(stream);
-    const MsgLayout L = msg_layout(h, p);
-    const int n = h->plan.n, k0 = p * h->nb, jb = std::min(h->nb, n - k0);
-    const size_t es = elem_size(h->plan.prec);
-    const char *m = static_cast<const char *>(msg);
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->plan.ws.nmoves + p, m, sizeof(int),
-                                     cudaMemcpyDeviceToDevice, s));
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->hdr, m + 4, sizeof(int), cudaMemcpyDeviceToDevice, s));
-    dlu_merge_singular(&h->info->singular_col, h->hdr, s);
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(ipiv + k0, m + L.ipiv, sizeof(int) * jb,
-                                     cudaMemcpyDeviceToDevice, s));
-    MPIRG_CUDA_CHECK(cudaMemcpyAsync(h->plan.ws.moves + (size_t)p * 2 * h->nb, m + L.moves,
-                                     sizeof(int2) * 2 * h->nb, cudaMemcpyDeviceToDevice, s));
-    MPIRG_CUDA_CHECK(cudaMemcpy2DAsync(static_cast<char *>(a) + ((size_t)k0 * n + k0) * es,
-                                       (size_t)n * es, m + L.panel, (n - k0) * es,
-                                       (n - k0) * es, jb, cudaMemcpyDeviceToDevice, s));
+    unpack_on(h, a, p, ipiv, msg, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// The whole distributed LU of one rank, driven from here so that no host
+// round trip sits between a panel and its broadcast: per panel p the owner
+// factors it on the critical stream, packs it and the communication stream
+// broadcasts it (NCCL over NVLink through `bcast`; the other ranks unpack it
+// on their communication stream), then every rank updates its own columns.
+// binary32 factors at nb = 64 run the single-GPU LU's paired TMA schedule
+// (dlu_f32_*, lu.cu); other precisions the per-step schedule of
+// mpirg_dlu_update with the same look-ahead as dist.factor.
+int mpirg_dlu_factor(mpirg_dlu *h, void *a, int *ipiv, int *perm, mpirg_bcast_fn bcast,
+                     void *ctx, void *stream, int *singular_col, mpirg_error *err)
+{
+  return guarded(err, [&] {
+    MPIRG_CUDA_CHECK(cudaSetDevice(h->device));
+    auto caller = static_cast<cudaStream_t>(stream);
+    DluPlan &d = h->plan;
+    const int np = h->np, G = d.G, r = d.r;
+    if (G > 1 && !bcast)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "a multi-rank LU needs a broadcast hook"};
+    if (G > 1 && !h->msg[0])
+      for (int i = 0; i < 2; ++i)
+      {
+        h->msg[i] = dalloc_bytes(msg_layout(h, 0).total);  // panel 0 is the tallest
+        MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&h->packed[i], cudaEventDisableTiming));
+      }
+    auto bc = [&](void *msg, int p, int owner, cudaStream_t s) {
+      if (bcast(ctx, msg, msg_layout(h, p).total, owner, s) != 0)
+        throw ApiError{MPIRG_ERR_NCCL, "broadcast of a factored panel failed"};
+    };
+    reset_info(h->info, caller);
+    if (dlu_f32_supported(d, a))
+    {
+      dlu_f32_begin(d, a, perm, caller);
+      cudaStream_t crit = dlu_f32_crit(d), comm = dlu_f32_comm(d);
+      cudaEvent_t *slot_free = static_cast<cudaEvent_t *>(d.cevents);
+      for (int p = 0; p < np; ++p)
+      {
+        const int owner = mpirg_dlu_owner(h, p), sl = p & 1;
+        if (owner == r)
+        {
+          dlu_panel(d, a, p, ipiv, h->info, crit);
+          dlu_f32_panel_ready(d, p, crit);
+          if (G > 1)
+          {
+            MPIRG_CUDA_CHECK(cudaStreamWaitEvent(crit, slot_free[sl], 0));
+            pack_on(h, a, p, ipiv, h->msg[sl], crit);
+            MPIRG_CUDA_CHECK(cudaEventRecord(h->packed[sl], crit));
+            MPIRG_CUDA_CHECK(cudaStreamWaitEvent(comm, h->packed[sl], 0));
+            bc(h->msg[sl], p, owner, comm);
+            MPIRG_CUDA_CHECK(cudaEventRecord(slot_free[sl], comm));
+          }
+        }
+        else
+        {
+          bc(h->msg[sl], p, owner, comm);
+          unpack_on(h, a, p, ipiv, h->msg[sl], comm);
+          dlu_f32_panel_ready(d, p, comm);
+          MPIRG_CUDA_CHECK(cudaEventRecord(slot_free[sl], comm));
+        }
+        dlu_f32_step(d, p, perm, owner == r);
+      }
+      dlu_f32_end(d, caller);
+    }
+    else
+    {
+      dlu_begin(d, perm, caller);
+      bool early = false;  // panel p was factored during step p-1 (look-ahead)
+      for (int p = 0; p < np; ++p)
+      {
+        const int owner = mpirg_dlu_owner(h, p);
+        if (owner == r)
+        {
+          if (!early)
+            dlu_panel(d, a, p, ipiv, h->info, caller);
+          if (G > 1)
+            pack_on(h, a, p, ipiv, h->msg[0], caller);
+        }
+        if (G > 1)
+        {
+          bc(h->msg[0], p, owner, caller);
+          if (owner != r)
+            unpack_on(h, a, p, ipiv, h->msg[0], caller);
+        }
+        early = false;
+        if (p + 1 < np && mpirg_dlu_owner(h, p + 1) == r)
+        {
+          dlu_update(d, a, p, 1, perm, caller);
+          dlu_panel(d, a, p + 1, ipiv, h->info, caller);
+          early = true;
+          dlu_update(d, a, p, 2, perm, caller);
+        }
+        else
+          dlu_update(d, a, p, 2, perm, caller);
+      }
+      dlu_end(d, caller);
+    }
+    int sc = INT_MAX;
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(&sc, &h->info->singular_col, sizeof(int),
+                                     cudaMemcpyDeviceToHost, caller));
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(caller));
+    if (singular_col)
+      *singular_col = sc == INT_MAX ? -1 : sc;
   });
 }
 

@@ -6,6 +6,7 @@
 // default) it costs one branch per launch.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -46,6 +47,23 @@ cudaEvent_t take()
 }  // namespace
 
 bool prof_on() { return g_on; }
+
+extern "C" char **environ;
+bool tool_attached()
+{
+  static const bool v = [] {
+    if (const char *e = std::getenv("MPIRG_TOOL_ATTACHED"))  // explicit override (tests)
+      return std::atoi(e) != 0;
+    for (char **e = environ; e && *e; ++e)
+      for (const char *k : {"CUDA_INJECTION64_PATH=", "CUDA_INJECTION32_PATH=",
+                            "NV_COMPUTE_PROFILER_", "NV_SANITIZER_", "NSYS_PROFILING_SESSION_ID=",
+                            "NV_NSIGHT_INJECTION_"})
+        if (std::strncmp(*e, k, std::strlen(k)) == 0)
+          return true;
+    return false;
+  }();
+  return v;
+}
 
 void prof_begin(int kind, cudaStream_t s)
 {

@@ -274,12 +274,12 @@ void residual_tma_launch(const ResidualPlan &p, const void *x, const void *b, vo
   constexpr int ST = 4;
   const int n = p.n;
   const int smem = res_stages_smem<ST, RPW>(sizeof(TW));
-  static bool configured = false;
-  if (!configured)
+  static DeviceOnce configured;
+  if (configured.needed())
   {
     MPIRG_CUDA_CHECK(cudaFuncSetAttribute(residual_tma_kernel<TW, TR, ST, RPW>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
+    configured.done();
   }
   CUtensorMap map;
   std::memcpy(&map, static_cast<const CUtensorMap *>(p.tmap) + (RPW == 32 ? 0 : RPW == 16 ? 1 : 2),

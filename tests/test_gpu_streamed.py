@@ -120,3 +120,39 @@ def test_streamed_refactor_graph_replay_reads_current_host_data(gpulib):
             assert same_bits(got[0], want[0])
             np.testing.assert_array_equal(got[1], want[1])
             assert got[2] == want[2]
+
+
+def test_streamed_graph_survives_scal_reallocation(gpulib):
+    """A solve with litmax above anything seen so far reallocates the handle's
+    scalar slots; the captured streamed-refactor graph had the old ||A||_1 slot
+    baked in, so it must be dropped (the replay used to write freed memory and
+    a_norm1 came back 0, changing the stopping test)."""
+    import torch
+    from paper_2311_14616_b200 import _lib as L
+    m = mirror()
+    n = 1024
+    a = greens(n, 800.0)
+    b = normal_vector(n, 0)
+    f = m.Factorization(a, working="double", factor="single", resid_term=False)
+    want_norm = f.a_norm1
+    want = f.solve(b, ce=10.0, litmax=40)
+    buf = torch.empty(n * n, dtype=torch.float64).pin_memory()
+    buf.numpy()[:] = np.asfortranarray(a).ravel(order="F")
+    err = L.mpirg_error()
+
+    def refactor():
+        st = lib().mpirg_factorization_refactor(f._h, C.c_void_p(buf.data_ptr()), 0, C.byref(err))
+        L.check(st, err)
+
+    f2 = m.Factorization(a, working="double", factor="single", resid_term=False)
+    f = f2  # a fresh handle whose scalar slots still have the default capacity
+    refactor()
+    refactor()  # captured
+    refactor()  # replayed
+    got = f.solve(b, ce=10.0, litmax=40)  # litmax > 16: slots reallocated
+    refactor()
+    assert f.a_norm1 == want_norm
+    again = f.solve(b, ce=10.0, litmax=40)
+    for g in (got, again):
+        assert g["reason"] == want["reason"] and g["rhist"] == want["rhist"]
+        assert np.array_equal(g["x"].view(np.uint64), want["x"].view(np.uint64))
