@@ -152,6 +152,16 @@ PROTOTYPES = {
     "mpirg_dlu_unpack": (_I, [_H, _P, _I, _P, _P, _P, _E]),
     "mpirg_dlu_update": (_I, [_H, _P, _I, _I, _P, _P, _E]),
     "mpirg_dlu_end": (_I, [_H, _P, C.POINTER(C.c_int), _E]),
+    "mpirg_dlu_factor": (_I, [_H, _P, _P, _P, _P, _P, _P, C.POINTER(C.c_int), _E]),
+    "mpirg_comm_unique_id": (_I, [_P, _E]),
+    "mpirg_comm_create": (_I, [C.POINTER(_H), _I, _I, _P, _I, _E]),
+    "mpirg_comm_destroy": (None, [_H]),
+    "mpirg_comm_nranks": (_I, [_H]),
+    "mpirg_comm_rank": (_I, [_H]),
+    "mpirg_comm_version": (_I, []),
+    "mpirg_comm_bcast": (_I, [_P, _P, _S, _I, _P]),
+    "mpirg_comm_send": (_I, [_H, _P, _S, _I, _P]),
+    "mpirg_comm_recv": (_I, [_H, _P, _S, _I, _P]),
     "mpirg_batch_ir_solve": (_I, [_I, _I, C.POINTER(mpirg_config), _P, _P, _I,
                                   C.POINTER(mpirg_term_params), _P, _P, _P, _I, _P, _P, _P,
                                   C.POINTER(C.c_double), _E]),
@@ -170,6 +180,9 @@ PROTOTYPES = {
     "mpirg_gen_integral_rhs": (None, [_I, _D, _P]),
     "mpirg_gen_matvec_compensated_f64": (None, [_I, _P, _P, _P]),
 }
+
+# mpirg_bcast_fn: the distributed LU's broadcast hook
+BCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
 
 _lib = None
 

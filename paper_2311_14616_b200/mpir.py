@@ -283,13 +283,41 @@ def solve(a, b, *, working="double", factor=None, residual=None, on_the_fly=None
 
 def batch_solve(a, b, *, working="double", factor=None, residual=None, on_the_fly=None,
                 resid_term=True, cr=None, ce=None, rmax=None, litmax=None, device=None,
-                raise_on_error=True) -> list[dict]:
+                devices=None, raise_on_error=True) -> list[dict]:
     """Config 5b: ``count`` independent systems, each exactly one
     MPFactorization + ir_solve_report (concurrent solves use
     separate objects). ``a``: (count, n, n) float64 (row-major matrices) or a
     CUDA tensor of TW holding count column-major n*n blocks; ``b``: (count, n).
-    The systems run concurrently on the device (mpirg_batch_ir_solve)."""
+    The systems run concurrently on the device (mpirg_batch_ir_solve).
+    ``devices=[d0, d1, ...]`` (host arrays only) shards the batch one
+    contiguous slice per listed GPU with no collective -- the slices run from
+    one host thread each and the reports come back in system order."""
     torch = _torch()
+    if devices is not None and len(devices) > 1:
+        if isinstance(a, torch.Tensor):
+            raise InvalidParameter("devices=[...] takes host arrays (each slice is copied to "
+                                   "its own GPU)")
+        from concurrent.futures import ThreadPoolExecutor
+
+        from .dist import batch_slice
+        a = np.asarray(a, dtype=np.float64)
+        b = np.asarray(b, dtype=np.float64)
+        count = a.shape[0]
+        kw = dict(working=working, factor=factor, residual=residual, on_the_fly=on_the_fly,
+                  resid_term=resid_term, cr=cr, ce=ce, rmax=rmax, litmax=litmax,
+                  raise_on_error=raise_on_error)
+
+        def one(i):
+            lo, hi = batch_slice(count, len(devices), i)
+            if hi <= lo:
+                return []
+            with torch.cuda.device(int(devices[i])):
+                return batch_solve(a[lo:hi], b[lo:hi], device=int(devices[i]), **kw)
+        with ThreadPoolExecutor(len(devices)) as ex:
+            parts = list(ex.map(one, range(len(devices))))
+        return [rep for part in parts for rep in part]
+    if devices is not None and len(devices) == 1:
+        device = devices[0]
     tp = update_parms(cr, ce, rmax, litmax)
     cfg = resolve_config(parse_precision(working),
                          None if factor is None else parse_precision(factor),

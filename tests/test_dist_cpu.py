@@ -105,3 +105,64 @@ def test_ownership_map():
     cols = sorted(c for bl in blocks for lo, hi in bl for c in range(lo, hi))
     assert cols == list(range(1000))
     assert blocks[1][0] == (128, 256) and blocks[0][-1] == (768, 896)
+
+
+def _batch_worker(rank, world, port, count, n, out):
+    import torch.distributed as dist
+
+    import helpers
+    import oracle
+    from paper_2311_14616_b200 import dist as D
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        orc = oracle.restatement()
+
+        def make_slice(lo, hi):
+            a = np.stack([helpers.diag_dominant(n, i, float(n)) for i in range(lo, hi)])
+            return a, np.ones((hi - lo, n))
+
+        def cpu_stand_in(a, b, **kw):  # the oracle in place of mpir.batch_solve
+            reps = []
+            for ai, bi in zip(a, b):
+                r = orc.ir(0, 1, 0, np.asfortranarray(ai), bi, resid_term=False, ce=10.0,
+                           litmax=10)
+                reps.append({"x": r["x"], "rhist": list(r["rhist"]), "reason": r["reason"]})
+            return reps
+        got = D.batch_solve_sliced(make_slice, count, D.Comm(), solver=cpu_stand_in)
+        if rank == 0:
+            np.savez(out, x=np.stack([g["x"] for g in got]),
+                     nr=np.array([len(g["rhist"]) for g in got]))
+        else:
+            assert got is None
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_slices_concatenate_in_system_order(tmp_path):
+    """Config 5b's multi-rank path (dist.batch_solve_sliced): contiguous slices,
+    no collective on the systems, reports gathered to rank 0 in system order.
+    The device solver is replaced by the oracle so the plumbing runs under gloo."""
+    import helpers
+    import oracle
+    count, n, world = 5, 48, 2
+    out = str(tmp_path / "b.npz")
+    mp.start_processes(_batch_worker, args=(world, _free_port(), count, n, out), nprocs=world,
+                       join=True, start_method="spawn")
+    got = np.load(out)
+    orc = oracle.restatement()
+    for i in range(count):
+        r = orc.ir(0, 1, 0, np.asfortranarray(helpers.diag_dominant(n, i, float(n))), np.ones(n),
+                   resid_term=False, ce=10.0, litmax=10)
+        assert np.array_equal(got["x"][i].view(np.uint64), r["x"].view(np.uint64))
+        assert got["nr"][i] == len(r["rhist"])
+
+
+def test_batch_slice_partition():
+    from paper_2311_14616_b200 import dist as D
+    for count, world in ((4096, 8), (5, 2), (3, 4), (0, 2)):
+        parts = [D.batch_slice(count, world, r) for r in range(world)]
+        assert parts[0][0] == 0 and parts[-1][1] == count
+        assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+        sizes = [hi - lo for lo, hi in parts]
+        assert max(sizes) - min(sizes) <= 1
