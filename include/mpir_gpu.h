@@ -212,6 +212,12 @@ int mpirg_residual(int tw, int tr, int n, const void *a, const void *x, const vo
  * L21 U12) with the 64-term product accumulated in fp32 on tcgen05.
  * a: n x n binary16 bits, column-major, n % 8 == 0. Exposed for testing. */
 int mpirg_tc_update(int n, void *a, int k0, int cb, int ce, void *stream, mpirg_error *err);
+/* The general K5b update the recursive tensor-core LU is built from:
+ * A[r0:r1, cb:ce] = fp16(fp32(A[r0:r1, cb:ce]) - A[r0:r1, k0:k0+K] A[k0:k0+K, cb:ce]),
+ * K a multiple of 64, ranges disjoint as in a right-looking LU
+ * (k0 + K <= r0, k0 + K <= cb). Exposed for testing. */
+int mpirg_tc_gemm(int n, void *a, int r0, int r1, int cb, int ce, int k0, int K, void *stream,
+                  mpirg_error *err);
 
 /* ---------------------------------------------------------------------------
  * Batched independent systems (BASELINE config 5b): count systems of size n,

@@ -139,6 +139,7 @@ PROTOTYPES = {
                                          C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "mpirg_factorization_set_factored": (_I, [_H, _I, _E]),
     "mpirg_tc_update": (_I, [_I, _P, _I, _I, _I, _P, _E]),
+    "mpirg_tc_gemm": (_I, [_I, _P, _I, _I, _I, _I, _I, _I, _P, _E]),
     "mpirg_dlu_create": (_I, [C.POINTER(_H), _I, _I, _I, _I, _I, _I, _I, _E]),
     "mpirg_dlu_destroy": (None, [_H]),
     "mpirg_dlu_nb": (_I, [_H]),

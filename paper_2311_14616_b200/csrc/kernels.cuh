@@ -99,6 +99,8 @@ struct LuWorkspace
   int *pp = nullptr;      // [n] composed row map of a tall panel
   int2 *smv = nullptr;    // [2*nb] row moves of the tall panel's 8-column leaves
   int *snm = nullptr;     // [nb/8]
+  int *zero = nullptr;    // one int, always 0 ("no row moves" for solve-only U12 launches)
+  float *pf32 = nullptr;  // [n][nb] binary32 copy of the current panel (lu_mode TC)
   void *ut = nullptr;     // float[2*nb][n]: transposed U12 of two steps (binary32)
   // late columns (launch_lu_late): panel snapshots, per-chunk U12 copies,
   // per-chunk streams and events; sized for late_n
@@ -146,11 +148,16 @@ struct TcPlan
 {
   alignas(64) unsigned char mapA[128];  // CUtensorMap: L21 boxes (64 rows x 64 k)
   alignas(64) unsigned char mapB[128];  // CUtensorMap: U12 boxes (64 k x 256 cols)
+  alignas(64) unsigned char mapB128[128];  // 64 k x 128 cols
+  alignas(64) unsigned char mapB64[128];   // 64 k x 64 cols
   void *a = nullptr;
   int n = 0;
 };
 bool tc_update_supported(int n, int nb);
 void tc_plan_make(TcPlan &p, void *a, int n);
+// rows [r0, r1) x columns [cb, ce) -= L[:, k0..k0+K) U[k0..k0+K, :) on tcgen05
+// (fp32 accumulation, one rounding to binary16); K a multiple of 64.
+void tc_gemm(const TcPlan &p, int r0, int r1, int cb, int ce, int k0, int K, cudaStream_t s);
 void launch_gemm_tc(const TcPlan &p, int k0, int cb, int ce, cudaStream_t s);
 
 // One rank of the 1-D block-cyclic LU (config 5a). a is the

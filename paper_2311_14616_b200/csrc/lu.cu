@@ -935,6 +935,159 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
   MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * np + np - 1], 0));
 }
 
+// ---- binary16 tensor-core schedule (lu_mode TC): recursive LU ---------------
+// factor(K0, w) factors columns [K0, K0 + w), rows [K0, n):
+//   w <= 64:  one panel (cluster kernel), which records its row moves;
+//   else:     factor the left half; apply its panels' row moves to the right
+//             half; U12 = L11^-1 A12 (recursive: 64-row solves + tensor-core
+//             updates); A22 -= L21 U12 on the tensor cores with K = w/2;
+//             factor the right half; apply its row moves to the left half's L.
+// Every update is one tcgen05 GEMM (lu_tc.cu) whose K doubles with each level:
+// 7/8 of the 2n^3/3 flops run at K >= n/16, and the trailing matrix is read and
+// written log2(n/64) times instead of n/64 times. The panels are factored in
+// binary32 (the binary16 panel converted into a scratch buffer, the binary32
+// cluster kernel, one rounding back): half the binary16 kernel's time, and no
+// less accurate. Not bitwise (lu_mode EXACT is); pivots are the reference's
+// whenever no near-tie is decided differently by the higher precision.
+__global__ void cvt_panel_h2f_kernel(const h16 *__restrict__ a, float *__restrict__ pf, int n,
+                                     int k0, int jb)
+{
+  const int rows = n - k0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)rows * jb;
+       i += (long)gridDim.x * blockDim.x)
+  {
+    const int c = (int)(i / rows), r = k0 + (int)(i - (long)c * rows);
+    pf[(size_t)c * n + r] = h2f(a[(size_t)(k0 + c) * n + r]);
+  }
+}
+
+__global__ void cvt_panel_f2h_kernel(const float *__restrict__ pf, h16 *__restrict__ a, int n,
+                                     int k0, int jb)
+{
+  const int rows = n - k0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)rows * jb;
+       i += (long)gridDim.x * blockDim.x)
+  {
+    const int c = (int)(i / rows), r = k0 + (int)(i - (long)c * rows);
+    a[(size_t)(k0 + c) * n + r] = f2h(pf[(size_t)c * n + r]);
+  }
+}
+
+static bool tc_panel_f32()
+{
+  static const bool v = [] {
+    const char *e = std::getenv("MPIRG_TC_PANEL");
+    return !(e && std::string(e) == "f16");
+  }();
+  return v;
+}
+
+struct TcRun
+{
+  h16 *a;
+  int n;
+  int *ipiv, *perm;
+  LuWorkspace *ws;
+  DevInfo *info;
+  cudaStream_t s;
+  const TcPlan *tc;
+};
+
+static int tc_split(int w) { return ((w / 64 + 1) / 2) * 64; }
+
+static void tc_panel(TcRun &R, int k0, int jb)
+{
+  LuWorkspace &ws = *R.ws;
+  const int p = k0 / 64, n = R.n;
+  int2 *mv = ws.moves + (size_t)p * 128;
+  int *nm = ws.nmoves + p;
+  if (ws.pf32 && tc_panel_f32() && panel_rpt<float, 64>(n - k0) > 0)
+  {
+    const long tot = (long)(n - k0) * jb;
+    const int g = (int)std::min<long>(148 * 4, (tot + 255) / 256);
+    prof_begin(KC_PANEL, R.s);
+    cvt_panel_h2f_kernel<<<g, 256, 0, R.s>>>(R.a, ws.pf32, n, k0, jb);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+    prof_end(KC_PANEL, R.s);
+    // the panel kernel addresses column k0 + c at a[(k0 + c) n + row]
+    launch_panel<float, 64>(ws.pf32 - (size_t)k0 * n, n, k0, jb, R.ipiv, mv, nm, R.info, R.s);
+    prof_begin(KC_PANEL, R.s);
+    cvt_panel_f2h_kernel<<<g, 256, 0, R.s>>>(ws.pf32, R.a, n, k0, jb);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+    prof_end(KC_PANEL, R.s);
+  }
+  else
+    panel_any<h16, 64>(R.a, n, k0, jb, R.ipiv, mv, nm, ws, R.info, R.s);
+  // the accumulated permutation follows on the side stream, off the chain
+  if (R.perm)
+  {
+    cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);
+    cudaStream_t side = static_cast<cudaStream_t>(ws.side);
+    MPIRG_CUDA_CHECK(cudaEventRecord(ev[p], R.s));
+    MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, ev[p], 0));
+    launch_moves<h16, 64>(R.a, n, 0, 0, ColMap{}, mv, nm, R.perm, side);
+  }
+}
+
+// row moves of panels [pa, pb), in order, on columns [cb, ce)
+static void tc_moves(TcRun &R, int pa, int pb, int cb, int ce)
+{
+  for (int p = pa; p < pb; ++p)
+    launch_moves<h16, 64>(R.a, R.n, cb, ce, ColMap{}, R.ws->moves + (size_t)p * 128,
+                          R.ws->nmoves + p, nullptr, R.s);
+}
+
+// rows [K0, K0 + sz) of columns [cb, ce) <- L11^-1 (those rows), L11 unit lower at (K0, K0)
+static void tc_trsm(TcRun &R, int K0, int sz, int cb, int ce)
+{
+  if (sz <= 64)
+  {
+    launch_mt<h16, 64>(R.a, R.n, K0, sz, cb, ce, ColMap{}, R.ws->moves, R.ws->zero, R.s);
+    return;
+  }
+  const int h = tc_split(sz);
+  tc_trsm(R, K0, h, cb, ce);
+  tc_gemm(*R.tc, K0 + h, K0 + sz, cb, ce, K0, h, R.s);
+  tc_trsm(R, K0 + h, sz - h, cb, ce);
+}
+
+static void tc_factor(TcRun &R, int K0, int w)
+{
+  if (w <= 64)
+  {
+    tc_panel(R, K0, w);
+    return;
+  }
+  const int h = tc_split(w);
+  tc_factor(R, K0, h);
+  tc_moves(R, K0 / 64, (K0 + h) / 64, K0 + h, K0 + w);
+  tc_trsm(R, K0, h, K0 + h, K0 + w);
+  tc_gemm(*R.tc, K0 + h, R.n, K0 + h, K0 + w, K0, h, R.s);
+  tc_factor(R, K0 + h, w - h);
+  tc_moves(R, (K0 + h) / 64, (K0 + w + 63) / 64, K0, K0 + h);
+}
+
+static void lu_run_tc(h16 *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                      cudaStream_t s, const TcPlan &tc)
+{
+  cudaStream_t side = static_cast<cudaStream_t>(ws.side);
+  cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);
+  const int np = ws.npanels;
+  if (perm)
+  {
+    ProfScope ps(KC_VEC, s);
+    iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(perm, n);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  }
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(ws.nmoves, 0, sizeof(int) * np, s));
+  MPIRG_CUDA_CHECK(cudaEventRecord(ev[np], s));
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(side, ev[np], 0));
+  TcRun R{a, n, ipiv, perm, &ws, info, s, &tc};
+  tc_factor(R, 0, n);
+  MPIRG_CUDA_CHECK(cudaEventRecord(ev[np + 1], side));
+  MPIRG_CUDA_CHECK(cudaStreamWaitEvent(s, ev[np + 1], 0));
+}
+
 // ---- binary32 single-GPU schedule: TMA trailing update, paired steps ------
 // MPIRG_GEMM=v4 keeps the one-step-per-pass schedule of lu_run (A/B runs).
 static int f32_mode()
@@ -1786,6 +1939,10 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.snm, sizeof(int) * (size_t)ws.nb));
   if (prec == B32 && ws.nb == 64 && n % 4 == 0)  // transposed U12 of two steps (lu_run_f32)
     MPIRG_CUDA_CHECK(cudaMalloc(&ws.ut, sizeof(float) * 2 * (size_t)ws.nb * n));
+  MPIRG_CUDA_CHECK(cudaMalloc(&ws.zero, sizeof(int)));
+  MPIRG_CUDA_CHECK(cudaMemset(ws.zero, 0, sizeof(int)));
+  if (prec == B16 && ws.nb == 64)  // binary32 copy of the current panel (lu_run_tc)
+    MPIRG_CUDA_CHECK(cudaMalloc(&ws.pf32, sizeof(float) * (size_t)ws.nb * std::max(1, n)));
   cudaStream_t side;
   // The side stream carries the bulk trailing update; give it the lowest
   // priority so the block scheduler hands freed SMs to the critical chain
@@ -1818,7 +1975,7 @@ void lu_workspace_free(LuWorkspace &ws)
   if (ws.moves)
     lu_graph_forget(ws.moves);
   for (void *p : {(void *)ws.moves, (void *)ws.nmoves, (void *)ws.pp, (void *)ws.smv,
-                  (void *)ws.snm, ws.ut})
+                  (void *)ws.snm, ws.ut, (void *)ws.zero, (void *)ws.pf32})
     if (p)
       cudaFree(p);
   if (ws.events)
@@ -1878,7 +2035,10 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
   {
     TcPlan plan;
     tc_plan_make(plan, a, n);
-    lu_dispatch<h16>(ws.nb, static_cast<h16 *>(a), n, ipiv, perm, ws, info, s, &plan);
+    if (std::getenv("MPIRG_TC_SCHEDULE") && std::string(std::getenv("MPIRG_TC_SCHEDULE")) == "flat")
+      lu_dispatch<h16>(ws.nb, static_cast<h16 *>(a), n, ipiv, perm, ws, info, s, &plan);  // K = 64
+    else
+      lu_run_tc(static_cast<h16 *>(a), n, ipiv, perm, ws, info, s, plan);
     return;
   }
   if (prec == B64)

@@ -1719,3 +1719,17 @@ int mpirg_tc_update(int n, void *a, int k0, int cb, int ce, void *stream, mpirg_
     launch_gemm_tc(plan, k0, cb, ce, static_cast<cudaStream_t>(stream));
   });
 }
+
+int mpirg_tc_gemm(int n, void *a, int r0, int r1, int cb, int ce, int k0, int K, void *stream,
+                  mpirg_error *err)
+{
+  return guarded(err, [&] {
+    if (!tc_update_supported(n, 64) || K <= 0 || K % 64 || k0 < 0 || k0 + K > r0 ||
+        k0 + K > cb || r1 > n || ce > n || r0 > r1 || cb > ce)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "unsupported TC update geometry"};
+    require_gpu();
+    TcPlan plan;
+    tc_plan_make(plan, a, n);
+    tc_gemm(plan, r0, r1, cb, ce, k0, K, static_cast<cudaStream_t>(stream));
+  });
+}

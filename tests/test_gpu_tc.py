@@ -57,6 +57,74 @@ def test_tc_update_kernel(gpulib, n, k0, cb, ce):
     assert torch.equal(untouched.view(torch.int16), a.view(torch.int16))
 
 
+@pytest.mark.parametrize("n,r0,r1,cb,ce,k0,K", [
+    (1024, 512, 1024, 512, 1024, 0, 512),      # 128 x 256 tiles, 8 stages of k
+    (1024, 256, 700, 320, 1000, 64, 192),      # ragged rows and columns
+    (2048, 1024, 2048, 1024, 1088, 0, 1024),   # 64-column tiles (narrow right half)
+    (2048, 1024, 2048, 1024, 1152, 512, 512),  # 128-column tiles
+    (2048, 64, 128, 128, 2048, 0, 64),         # short and wide (inside the U12 solve)
+    (8192, 4096, 8192, 4096, 8192, 2048, 2048),  # 256 x 256 tiles (both accumulators)
+])
+def test_tc_gemm_general(gpulib, n, r0, r1, cb, ce, k0, K):
+    """The persistent tcgen05 update at the shapes the recursive LU issues,
+    against an fp64 product on the device: within one binary16 ulp of the
+    rounded result plus the fp32 accumulation error; everything outside
+    [r0:r1, cb:ce] untouched."""
+    import torch
+
+    from paper_2311_14616_b200 import _lib as L
+    g = torch.Generator().manual_seed(n + K + r0)
+    a = (torch.randn(n, n, generator=g) * (0.5 / max(1.0, (K / 64) ** 0.5))).half().cuda()
+    dev = a.clone()  # a[col, row]: column-major storage
+    err = L.mpirg_error()
+    st = L.lib().mpirg_tc_gemm(n, dev.data_ptr(), r0, r1, cb, ce, k0, K, None, C.byref(err))
+    L.check(st, err)
+    torch.cuda.synchronize()
+    Lm = a[k0:k0 + K, r0:r1].double()   # [k, rows]
+    Um = a[cb:ce, k0:k0 + K].double()   # [cols, k]
+    prod = Um @ Lm                      # [cols, rows]
+    cold = a[cb:ce, r0:r1].double()
+    want = (cold - prod).float().half()
+    tile = dev[cb:ce, r0:r1]
+    diff = (tile.double() - want.double()).abs().cpu().numpy()
+    mag = np.maximum(want.float().abs().cpu().numpy(), tile.float().abs().cpu().numpy())
+    absum = (cold.abs() + Um.abs() @ Lm.abs()).cpu().numpy()
+    assert np.all(diff <= _ulp16(mag) + K * 2.0 ** -24 * absum)
+    assert (diff == 0).mean() >= 0.98
+    untouched = dev.clone()
+    untouched[cb:ce, r0:r1] = a[cb:ce, r0:r1]
+    assert torch.equal(untouched.view(torch.int16), a.view(torch.int16))
+
+
+@pytest.mark.parametrize("kind,n", [("greens", 1024), ("randn", 1024), ("randn", 1984),
+                                    ("randn", 1000)])
+def test_tc_lu_backward_error(gpulib, kind, n):
+    """The recursive tensor-core LU (binary32 panels, tcgen05 updates) as a
+    factorization: ||P A - L U|| small against the binary16 unit roundoff, on a
+    diagonally dominant and on pivot-heavy matrices (row moves crossing every
+    level of the recursion), n not a power of two and not a multiple of 64."""
+    import torch
+
+    from helpers import greens, normal_matrix
+    from paper_2311_14616_b200 import kernels
+    a = greens(n, 1.0) if kind == "greens" else normal_matrix(n, 11) / np.sqrt(n)
+    ah = torch.from_numpy(np.asfortranarray(a).T.copy()).half().cuda()  # [col, row]
+    lu = ah.clone().reshape(-1)
+    ipiv = torch.zeros(n, dtype=torch.int32, device="cuda")
+    kernels.lu_factor(lu.view(torch.int16), ipiv, n, lu_mode=1)
+    lu = lu.reshape(n, n).double().T  # (row, col)
+    Lf = torch.tril(lu, -1) + torch.eye(n, dtype=torch.float64, device="cuda")
+    Uf = torch.triu(lu)
+    pa = ah.double().T.clone()
+    for k, p in enumerate(ipiv.cpu().tolist()):
+        if p != k:
+            pa[[k, p]] = pa[[p, k]]
+    resid = (pa - Lf @ Uf).abs().max().item()
+    scale = (Lf.abs() @ Uf.abs()).max().item()
+    assert resid <= 16 * 2.0 ** -11 * scale, (resid, scale)
+    assert torch.all(Lf.abs() <= 1.0 + 2.0 ** -9)  # partial pivoting held
+
+
 @pytest.mark.parametrize("n", [1024, pytest.param(8192, marks=pytest.mark.slow)])
 def test_tc_mode_solution_within_stopping_rule_bound(gpulib, n):
     from helpers import greens
