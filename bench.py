@@ -485,6 +485,31 @@ def run_ours(args, world, rank, local):
                                      "tflops": tfl.value, "peak_tflops": ffma.value,
                                      "frac": tfl.value / ffma.value})
 
+    # The tcgen05 update timed alone at the three largest node updates of the
+    # recursive LU (K = n/2, n/4, n/8 on the first block of each level).
+    tc_alone = []
+    if tc:
+        scratch = (torch.randn(n * n, device="cuda") * 0.01).half()
+        for K in (n // 2, n // 4, n // 8):
+            if K % 64 or K <= 0:
+                continue
+            tms = []
+            for i in range(4):
+                flush.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                L.check(lib.mpirg_tc_gemm(n, scratch.data_ptr(), K, n, K, n, 0, K, None,
+                                          C.byref(err)), err)
+                e1.record()
+                torch.cuda.synchronize()
+                if i:
+                    tms.append(e0.elapsed_time(e1))
+            tfl = 2.0 * (n - K) ** 2 * K / (min(tms) * 1e-3) / 1e12
+            tc_alone.append({"M": n - K, "N": n - K, "K": K, "ms": min(tms), "tflops": tfl,
+                             "peak_tflops": gemm_peak,
+                             "frac": tfl / gemm_peak if gemm_peak else None})
+        del scratch
+
     checks = None
     if big:
         # Size-independent properties at N = 65536 (the oracle would need hours):
@@ -526,6 +551,7 @@ def run_ours(args, world, rank, local):
             "iters": iters, "reason": reason,
             "roofline": roofline, "kernels": kernels,
             "ffma_peak_tflops": ffma.value, "update_kernel_alone": update_alone,
+            "tc_update_alone": tc_alone,
             "e2e": e2e, "gpu_launches": launches,
             "clocks": {**clocks.summary(),
                        "window": "warm-up, timed, profiled and e2e steps (nvidia-smi -lms 50)"},

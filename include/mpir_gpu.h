@@ -168,6 +168,16 @@ int mpirg_factorization_get_a_high(const mpirg_factorization *f, void *out_tw);
 const void *mpirg_factorization_a_high_device(const mpirg_factorization *f);
 const void *mpirg_factorization_packed_lu_device(const mpirg_factorization *f);
 const int *mpirg_factorization_ipiv_device(const mpirg_factorization *f);
+/* Preallocated solver state (mp_structures.hpp:186-192: residual_buf, sol_buf,
+ * comp_buf, low_buf, work_buf) as stable device pointers, n values each of
+ * TR / TR / TR / TF / TW. The refinement loop owns them during a solve.
+ * comp_buf is scratch only (the device residual keeps its compensation in
+ * registers); low_buf and work_buf alias the one substitution scratch. */
+void *mpirg_factorization_residual_buf_device(mpirg_factorization *f);
+void *mpirg_factorization_sol_buf_device(mpirg_factorization *f);
+void *mpirg_factorization_comp_buf_device(mpirg_factorization *f);
+void *mpirg_factorization_low_buf_device(mpirg_factorization *f);
+void *mpirg_factorization_work_buf_device(mpirg_factorization *f);
 /* The CUDA stream every call on this handle runs on (cudaStream_t). */
 void *mpirg_factorization_stream(const mpirg_factorization *f);
 

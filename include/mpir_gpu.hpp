@@ -12,6 +12,7 @@
 // Element types: double, float, and mpir::gpu::Half (binary16 bits).
 #pragma once
 
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -23,9 +24,43 @@
 
 #include "mpir_gpu.h"
 
+// With MPIR_GPU_USE_REFERENCE_TYPES defined (and the reference's proj/include
+// on the include path, -std=c++20) the twin uses the reference's own Matrix,
+// Half, TermParams / update_parms, StopReason, FactorOptions, PrecisionConfig
+// and exception classes instead of the restatements below, so a reference
+// program passes its mpir::Matrix objects straight in and catches the very
+// same exception types; only the device-backed classes remain here.
+#ifdef MPIR_GPU_USE_REFERENCE_TYPES
+#include "mpir/errors.hpp"
+#include "mpir/half.hpp"
+#include "mpir/ir_engine.hpp"
+#include "mpir/matrix.hpp"
+#include "mpir/mp_structures.hpp"
+#include "mpir/precision.hpp"
+#endif
+
 namespace mpir::gpu
 {
 
+#ifdef MPIR_GPU_USE_REFERENCE_TYPES
+using ::mpir::DimensionMismatch;
+using ::mpir::Error;
+using ::mpir::FactorOptions;
+using ::mpir::Half;
+using ::mpir::InvalidConfig;
+using ::mpir::InvalidParameter;
+using ::mpir::InvalidSize;
+using ::mpir::KrylovKind;
+using ::mpir::Matrix;
+using ::mpir::NonFiniteResult;
+using ::mpir::OverflowDetected;
+using ::mpir::Precision;
+using ::mpir::PrecisionConfig;
+using ::mpir::SingularPivot;
+using ::mpir::StopReason;
+using ::mpir::TermParams;
+using ::mpir::update_parms;
+#else
 // ---- exceptions (errors.hpp) ------------------------------------------------
 struct Error : std::runtime_error
 {
@@ -42,8 +77,9 @@ struct SingularPivot : Error
 };
 struct NonFiniteResult : Error
 {
-  NonFiniteResult(const std::string &m, std::vector<double> r, std::vector<double> d)
-    : Error(m), rhist(std::move(r)), dhist(std::move(d))
+  NonFiniteResult(const std::string &m, std::vector<double> r, std::vector<double> d,
+                  std::vector<int> k = {})
+    : Error(m), rhist(std::move(r)), dhist(std::move(d)), khist(std::move(k))
   {
   }
   std::vector<double> rhist, dhist;
@@ -65,6 +101,7 @@ struct InvalidSize : Error
 {
   using Error::Error;
 };
+#endif
 struct CudaError : Error
 {
   using Error::Error;
@@ -83,7 +120,7 @@ inline void throw_status(int st, const mpirg_error &e, std::vector<double> rh = 
     case MPIRG_ERR_SINGULAR:
       throw SingularPivot(m, e.column);
     case MPIRG_ERR_NONFINITE:
-      throw NonFiniteResult(m, std::move(rh), std::move(dh));
+      throw NonFiniteResult(m, std::move(rh), std::move(dh), std::vector<int>{});
     case MPIRG_ERR_DIMENSION:
       throw DimensionMismatch(m);
     case MPIRG_ERR_INVALID_CONFIG:
@@ -98,15 +135,18 @@ inline void throw_status(int st, const mpirg_error &e, std::vector<double> rh = 
 }
 
 // ---- element types ------------------------------------------------------------
+#ifndef MPIR_GPU_USE_REFERENCE_TYPES
 struct Half
 {
   std::uint16_t bits = 0;
 };
-template <typename T> struct precision_of;
-template <> struct precision_of<double> : std::integral_constant<int, MPIRG_B64> {};
-template <> struct precision_of<float> : std::integral_constant<int, MPIRG_B32> {};
-template <> struct precision_of<Half> : std::integral_constant<int, MPIRG_B16> {};
+#endif
+template <typename T> struct prec_code;
+template <> struct prec_code<double> : std::integral_constant<int, MPIRG_B64> {};
+template <> struct prec_code<float> : std::integral_constant<int, MPIRG_B32> {};
+template <> struct prec_code<Half> : std::integral_constant<int, MPIRG_B16> {};
 
+#ifndef MPIR_GPU_USE_REFERENCE_TYPES
 // ---- Matrix (matrix.hpp:19-61): column-major --------------------------------------
 template <typename T>
 class Matrix
@@ -170,6 +210,53 @@ enum class StopReason
   IterationLimit
 };
 
+struct FactorOptions
+{
+  bool resid_term = true;
+  std::optional<bool> on_the_fly;
+};
+
+// mpir::Precision (precision.hpp:20-25), PrecisionConfig (precision.hpp:210-231),
+// KrylovKind (mp_structures.hpp)
+enum class Precision
+{
+  B64,
+  B32,
+  B16
+};
+struct PrecisionConfig
+{
+  Precision tw = Precision::B64;
+  Precision tf = Precision::B32;
+  Precision tr = Precision::B64;
+  bool on_the_fly = false;
+  Precision ts() const { return on_the_fly ? tw : tf; }
+  void validate() const
+  {
+    // a smaller code is a wider format
+    if (static_cast<int>(tw) > static_cast<int>(tf))
+      throw InvalidConfig("factorization precision must not exceed the working precision");
+    if (static_cast<int>(tr) > static_cast<int>(tw))
+      throw InvalidConfig("residual precision must be at least the working precision");
+    if (tf == tw && !on_the_fly)
+      throw InvalidConfig("equal-precision factors require on-the-fly solves");
+  }
+};
+enum class KrylovKind
+{
+  None,
+  Gmres,
+  Bicgstab
+};
+#endif
+
+#ifdef MPIR_GPU_USE_REFERENCE_TYPES
+template <typename TW>
+struct SolveReport : ::mpir::SolveReport<TW>
+{
+  double device_ms = 0.0;
+};
+#else
 template <typename TW>
 struct SolveReport
 {
@@ -180,12 +267,7 @@ struct SolveReport
   bool breakdown = false;
   double device_ms = 0.0;
 };
-
-struct FactorOptions
-{
-  bool resid_term = true;
-  std::optional<bool> on_the_fly;
-};
+#endif
 
 // ---- MPFactorization (mp_structures.hpp:97-213) ------------------------------------
 template <typename TW, typename TF, typename TR = TW>
@@ -201,9 +283,9 @@ public:
     if (!a.square())
       throw DimensionMismatch("matrix must be square");
     mpirg_config c{};
-    c.tw = precision_of<TW>::value;
-    c.tf = precision_of<TF>::value;
-    c.tr = precision_of<TR>::value;
+    c.tw = prec_code<TW>::value;
+    c.tf = prec_code<TF>::value;
+    c.tr = prec_code<TR>::value;
     c.on_the_fly = opts.on_the_fly ? int(*opts.on_the_fly) : -1;
     c.resid_term = opts.resid_term ? 1 : 0;
     c.lu_mode = MPIRG_LU_EXACT;
@@ -266,6 +348,26 @@ public:
     mpirg_factorization_get_pivots(h_, v.data());
     return v;
   }
+  // Preallocated solver state (mp_structures.hpp:186-192) as stable DEVICE
+  // pointers, n values each; the refinement loop owns them during a solve.
+  // comp_buf is scratch only (the device residual keeps its compensation in
+  // registers); low_buf and work_buf alias the one substitution scratch (a
+  // configuration uses the scaled TF solve or the promoting TW solve, not both).
+  TR *residual_buf() { return static_cast<TR *>(mpirg_factorization_residual_buf_device(h_)); }
+  TR *sol_buf() { return static_cast<TR *>(mpirg_factorization_sol_buf_device(h_)); }
+  TR *comp_buf() { return static_cast<TR *>(mpirg_factorization_comp_buf_device(h_)); }
+  TF *low_buf() { return static_cast<TF *>(mpirg_factorization_low_buf_device(h_)); }
+  TW *work_buf() { return static_cast<TW *>(mpirg_factorization_work_buf_device(h_)); }
+  // Device views of the matrix copies (column-major n x n) and pivots.
+  const TW *a_high_device() const
+  {
+    return static_cast<const TW *>(mpirg_factorization_a_high_device(h_));
+  }
+  const TF *packed_lu_device() const
+  {
+    return static_cast<const TF *>(mpirg_factorization_packed_lu_device(h_));
+  }
+  const int *ipiv_device() const { return mpirg_factorization_ipiv_device(h_); }
   mpirg_factorization *handle() { return h_; }
 
 private:
@@ -332,5 +434,146 @@ std::vector<TR> residual_tr(MPFactorization<TW, TF, TR> &f, const std::vector<TW
   throw_status(mpirg_residual_tr(f.handle(), x.data(), b.data(), r.data(), 0, &e), e);
   return r;
 }
+
+// ---- AnyFactorization (runtime.hpp:34-68, runtime.cpp:67-134) ----------------------
+// The type-erased facade the reference's CLI and Python module call. The
+// C-ABI is already type-erased, so one handle covers every supported
+// precision combination. Input arrives in double and is rounded once into the
+// working precision (runtime.cpp:23-28,56-63; demote_checked's overflow rule,
+// precision.hpp:172-185).
+struct RuntimeReport
+{
+  std::vector<double> sol, rhist, dhist;
+  std::vector<int> khist;
+  StopReason reason = StopReason::IterationLimit;
+  bool breakdown = false;
+  double seconds = 0.0;
+};
+
+namespace detail
+{
+inline std::vector<float> to_b32(const double *v, std::size_t count)
+{
+  std::vector<float> out(count);
+  for (std::size_t i = 0; i < count; ++i)
+  {
+    const double x = v[i];
+    if (std::isfinite(x) && std::fabs(x) > 3.4028234663852886e38)
+      throw OverflowDetected("value " + std::to_string(x) +
+                             " exceeds the largest finite b32 value");
+    out[i] = static_cast<float>(x);
+  }
+  return out;
+}
+}  // namespace detail
+
+class AnyFactorization
+{
+public:
+  AnyFactorization(const Matrix<double> &a, const PrecisionConfig &cfg, bool resid_term = true,
+                   KrylovKind kind = KrylovKind::None, int basissize = 10, int device = -1)
+    : cfg_((cfg.validate(), cfg))  // validated before any allocation (runtime.cpp:69)
+  {
+    (void)basissize;
+    if (kind != KrylovKind::None)
+      throw InvalidParameter("Krylov corrections are not part of the B200 IR hot path");
+    if (cfg.tw == Precision::B16)
+      throw InvalidConfig("working precision must be b64 or b32");
+    if (a.rows() != a.cols())
+      throw DimensionMismatch("matrix must be square");
+    mpirg_config c{};
+    c.tw = static_cast<int>(cfg.tw);
+    c.tf = static_cast<int>(cfg.tf);
+    c.tr = static_cast<int>(cfg.tr);
+    c.on_the_fly = cfg.on_the_fly ? 1 : 0;
+    c.resid_term = resid_term ? 1 : 0;
+    c.lu_mode = MPIRG_LU_EXACT;
+    c.nb = 0;
+    c.device = device;
+    mpirg_error e{};
+    if (cfg.tw == Precision::B64)
+      throw_status(mpirg_factorization_create(&h_, a.rows(), &c, a.data(), 0, &e), e);
+    else
+    {
+      const auto a32 = detail::to_b32(a.data(), a.size());
+      throw_status(mpirg_factorization_create(&h_, a.rows(), &c, a32.data(), 0, &e), e);
+    }
+  }
+  AnyFactorization(const AnyFactorization &) = delete;
+  AnyFactorization &operator=(const AnyFactorization &) = delete;
+  AnyFactorization(AnyFactorization &&o) noexcept : cfg_(o.cfg_), h_(o.h_) { o.h_ = nullptr; }
+  ~AnyFactorization() { mpirg_factorization_destroy(h_); }
+
+  int n() const { return mpirg_factorization_n(h_); }
+  const PrecisionConfig &config() const { return cfg_; }
+
+  // Iterative refinement (runtime.cpp:78-103).
+  RuntimeReport solve(const std::vector<double> &b, const TermParams &tp = {})
+  {
+    if (static_cast<int>(b.size()) != n())
+      throw DimensionMismatch("right-hand side length does not match the matrix");
+    RuntimeReport out;
+    const int cap = tp.litmax + 1;
+    out.rhist.resize(cap > 0 ? cap : 1);
+    out.dhist.resize(cap > 0 ? cap : 1);
+    std::vector<float> b32, s32;
+    out.sol.resize(b.size());
+    const bool w64 = cfg_.tw == Precision::B64;
+    if (!w64)
+    {
+      b32 = detail::to_b32(b.data(), b.size());
+      s32.resize(b.size());
+    }
+    mpirg_report r{};
+    r.sol = w64 ? static_cast<void *>(out.sol.data()) : static_cast<void *>(s32.data());
+    r.sol_on_device = 0;
+    r.rhist = out.rhist.data();
+    r.dhist = out.dhist.data();
+    r.hist_capacity = cap;
+    const mpirg_term_params t{tp.cr, tp.ce, tp.rmax, tp.litmax};
+    mpirg_error e{};
+    const auto t0 = std::chrono::steady_clock::now();
+    const int st = mpirg_ir_solve(h_, w64 ? static_cast<const void *>(b.data())
+                                          : static_cast<const void *>(b32.data()),
+                                  0, &t, &r, &e);
+    const auto t1 = std::chrono::steady_clock::now();
+    out.rhist.resize(r.rhist_len);
+    out.dhist.resize(r.dhist_len);
+    throw_status(st, e, out.rhist, out.dhist);
+    if (!w64)
+      for (std::size_t i = 0; i < s32.size(); ++i)
+        out.sol[i] = s32[i];
+    out.reason = static_cast<StopReason>(r.reason);
+    out.seconds = std::chrono::duration<double>(t1 - t0).count();
+    return out;
+  }
+
+  // Krylov direct solves are outside the B200 hot path.
+  std::vector<double> direct_solve(const std::vector<double> &, KrylovKind = KrylovKind::Gmres,
+                                   int = 100, double = 1e-10, double * = nullptr)
+  {
+    throw InvalidParameter("Krylov direct solves are not part of the B200 IR hot path");
+  }
+
+  // Reuse the allocation for a new matrix of the same size (runtime.cpp:122-134).
+  void refactor(const Matrix<double> &a)
+  {
+    if (a.rows() != n() || a.cols() != n())
+      throw DimensionMismatch("refactor matrix has a different shape");
+    mpirg_error e{};
+    if (cfg_.tw == Precision::B64)
+      throw_status(mpirg_factorization_refactor(h_, a.data(), 0, &e), e);
+    else
+    {
+      const auto a32 = detail::to_b32(a.data(), a.size());
+      throw_status(mpirg_factorization_refactor(h_, a32.data(), 0, &e), e);
+    }
+  }
+  mpirg_factorization *handle() { return h_; }
+
+private:
+  PrecisionConfig cfg_;
+  mpirg_factorization *h_ = nullptr;
+};
 
 }  // namespace mpir::gpu

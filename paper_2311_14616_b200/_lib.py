@@ -126,6 +126,11 @@ PROTOTYPES = {
     "mpirg_factorization_packed_lu_device": (_P, [_H]),
     "mpirg_factorization_ipiv_device": (_P, [_H]),
     "mpirg_factorization_stream": (_P, [_H]),
+    "mpirg_factorization_residual_buf_device": (_P, [_H]),
+    "mpirg_factorization_sol_buf_device": (_P, [_H]),
+    "mpirg_factorization_comp_buf_device": (_P, [_H]),
+    "mpirg_factorization_low_buf_device": (_P, [_H]),
+    "mpirg_factorization_work_buf_device": (_P, [_H]),
     "mpirg_ir_solve": (_I, [_H, _P, _I, C.POINTER(mpirg_term_params), C.POINTER(mpirg_report), _E]),
     "mpirg_residual_tr": (_I, [_H, _P, _P, _P, _I, _E]),
     "mpirg_demote": (_I, [_I, _I, _S, _P, _P, C.POINTER(C.c_int), _P, _E]),

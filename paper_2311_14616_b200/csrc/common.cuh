@@ -210,6 +210,15 @@ __device__ __forceinline__ void st_release(int *p, int v)
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Batched launches (config 5b): system z = blockIdx.z of a launch works on
+// A + z*a, ipiv/perm + z*vec, moves + z*moves, nmoves + z*nm, info + z.
+// All zero (the default) is the single-system launch.
+struct BatchStride
+{
+  size_t a = 0;
+  int vec = 0, moves = 0, nm = 0, info = 0;
+};
+
 // Device-side error record shared by the kernels of one handle.
 struct DevInfo
 {

@@ -100,7 +100,6 @@ struct LuWorkspace
   int2 *smv = nullptr;    // [2*nb] row moves of the tall panel's 8-column leaves
   int *snm = nullptr;     // [nb/8]
   int *zero = nullptr;    // one int, always 0 ("no row moves" for solve-only U12 launches)
-  float *pf32 = nullptr;  // [n][nb] binary32 copy of the current panel (lu_mode TC)
   void *ut = nullptr;     // float[2*nb][n]: transposed U12 of two steps (binary32)
   // late columns (launch_lu_late): panel snapshots, per-chunk U12 copies,
   // per-chunk streams and events; sized for late_n
@@ -140,6 +139,12 @@ void launch_lu_late(void *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevIn
                     cudaStream_t s, const LuLate &late);
 void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWorkspace &ws,
                DevInfo *info, cudaStream_t s);
+// Config 5b: the binary32 LU of ns independent n x n systems stored back to
+// back (a + z n^2, ipiv/perm + z n, moves + z np 128, nmoves + z np, info + z),
+// one launch per step for the whole group (lu.cu).
+bool lu_batched_supported(int prec, int n);
+void launch_lu_batched_f32(float *a, int n, int ns, int *ipiv, int *perm, int2 *moves,
+                           int *nmoves, DevInfo *info, cudaStream_t s);
 // perm from ipiv for callers that only hold ipiv (standalone solves).
 void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s);
 
@@ -157,7 +162,8 @@ bool tc_update_supported(int n, int nb);
 void tc_plan_make(TcPlan &p, void *a, int n);
 // rows [r0, r1) x columns [cb, ce) -= L[:, k0..k0+K) U[k0..k0+K, :) on tcgen05
 // (fp32 accumulation, one rounding to binary16); K a multiple of 64.
-void tc_gemm(const TcPlan &p, int r0, int r1, int cb, int ce, int k0, int K, cudaStream_t s);
+void tc_gemm(const TcPlan &p, int r0, int r1, int cb, int ce, int k0, int K, cudaStream_t s,
+             int kclass = 4 /* KC_GEMM */);
 void launch_gemm_tc(const TcPlan &p, int k0, int cb, int ce, cudaStream_t s);
 
 // One rank of the 1-D block-cyclic LU (config 5a). a is the

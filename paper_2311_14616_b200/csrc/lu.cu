@@ -88,9 +88,15 @@ __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, 
                                                              int ce, ColMap map,
                                                              const int2 *__restrict__ moves,
                                                              const int *__restrict__ nmoves,
-                                                             int *__restrict__ perm)
+                                                             int *__restrict__ perm,
+                                                             BatchStride bs = BatchStride{})
 {
   constexpr int PER = (2 * NB + 31) / 32;
+  A += (size_t)blockIdx.z * bs.a;
+  moves += (size_t)blockIdx.z * bs.moves;
+  nmoves += (size_t)blockIdx.z * bs.nm;
+  if (perm)
+    perm += (size_t)blockIdx.z * bs.vec;
   const int nm = *nmoves;
   if (nm == 0)
     return;
@@ -146,6 +152,49 @@ __global__ void __launch_bounds__(256) lu_apply_moves_kernel(T *__restrict__ A, 
   }
 }
 
+// The row moves of several consecutive panels [pa, pb), applied in panel
+// order to the columns [cb, ce) -- one warp per column, so a column's moves
+// stay ordered without any grid-wide synchronisation (lu_run_tc applies a
+// whole sub-tree's moves to the other half of its block in one launch).
+template <typename T, int NB>
+__global__ void __launch_bounds__(256) lu_apply_moves_multi_kernel(
+    T *__restrict__ A, int n, int cb, int ce, const int2 *__restrict__ moves,
+    const int *__restrict__ nmoves, int pa, int pb)
+{
+  constexpr int PER = (2 * NB + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = pa; p < pb; ++p)
+  {
+    const int nm = nmoves[p];
+    if (nm == 0)
+      continue;  // warp-uniform
+    int2 mv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+    {
+      const int e = lane + 32 * q;
+      mv[q] = e < nm ? moves[(size_t)p * 2 * NB + e] : make_int2(-1, -1);
+    }
+    for (int c = cb + gw; c < ce; c += nw)
+    {
+      T *cp = A + (size_t)c * n;
+      T v[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q)
+        if (mv[q].x >= 0)
+          v[q] = cp[mv[q].y];
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < PER; ++q)
+        if (mv[q].x >= 0)
+          cp[mv[q].x] = v[q];
+      __syncwarp();
+    }
+  }
+}
+
 // Row moves + U12 = L11^{-1} A12 for the trailing columns [cb, ce).
 // CTA = 4 warps, 32 columns (8 per warp). Phase 1: each warp gathers the
 // moves of its 8 columns (lanes over move entries). Phase 2: each warp solves
@@ -158,11 +207,15 @@ template <typename T, int NB>
 __global__ void __launch_bounds__(128) lu_mt_kernel(T *__restrict__ A, int n, int k0, int jb,
                                                     int cb, int ce, ColMap map,
                                                     const int2 *__restrict__ moves,
-                                                    const int *__restrict__ nmoves)
+                                                    const int *__restrict__ nmoves,
+                                                    BatchStride bs = BatchStride{})
 {
   constexpr int PER = (2 * NB + 31) / 32;
   constexpr int RL = (NB + 31) / 32;  // panel rows per lane
   __shared__ T L[NB][NB + 1];
+  A += (size_t)blockIdx.z * bs.a;
+  moves += (size_t)blockIdx.z * bs.moves;
+  nmoves += (size_t)blockIdx.z * bs.nm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   {
     // stage L11 with all loads in flight before the stores
@@ -401,9 +454,11 @@ __global__ void __launch_bounds__(256) lu_gemm_kernel(T *__restrict__ A, int n, 
 // and takes one FMA per k, k ascending.
 template <int NB, int BM, int BN>
 __global__ void __launch_bounds__(256, 2) lu_gemm_v4_kernel(float *__restrict__ A, int n, int k0,
-                                                         int jb, int cb, int ce, ColMap map)
+                                                         int jb, int cb, int ce, ColMap map,
+                                                         size_t batch_stride = 0)
 {
   constexpr int TM = BM / 16, TN = BN / 16;
+  A += (size_t)blockIdx.z * batch_stride;
   constexpr int BPAD = 4;
   extern __shared__ __align__(16) unsigned char gsm[];
   float *As = reinterpret_cast<float *>(gsm);  // [NB][BM]
@@ -584,13 +639,13 @@ __global__ void compact_moves_kernel(const int *__restrict__ pp, int lo, int hi,
 
 __global__ void min_into_kernel(int *dst, const int *src) { *dst = min(*dst, *src); }
 
-template <typename T, int NB, int RPT, int NTX>
+template <typename T, int NB, int RPT, int NTX, typename TG = T>
 void configure_panel()
 {
   static DeviceOnce done;
   if (!done.needed())
     return;
-  auto k = panel2::lu_panel2_kernel<T, NB, RPT, NTX>;
+  auto k = panel2::lu_panel2_kernel<T, NB, RPT, NTX, TG>;
   MPIRG_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   MPIRG_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)panel2::panel_dyn_smem<T, NB, RPT, NTX>()));
@@ -620,13 +675,13 @@ static int panel_spec()
   return v;
 }
 
-template <typename T, int NB, int RPT, int NTX = panel2::NT>
-void launch_panel_rpt(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm,
-                      DevInfo *info, cudaStream_t s)
+template <typename T, int NB, int RPT, int NTX = panel2::NT, typename TG = T>
+void launch_panel_rpt(int cs, TG *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm,
+                      DevInfo *info, cudaStream_t s, int ns = 1, BatchStride bs = BatchStride{})
 {
-  configure_panel<T, NB, RPT, NTX>();
+  configure_panel<T, NB, RPT, NTX, TG>();
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cs);
+  cfg.gridDim = dim3(cs, 1, ns);
   cfg.blockDim = dim3(NTX);
   cfg.dynamicSmemBytes = panel2::panel_dyn_smem<T, NB, RPT, NTX>();
   cfg.stream = s;
@@ -637,8 +692,8 @@ void launch_panel_rpt(int cs, T *a, int n, int k0, int jb, int *ipiv, int2 *mv, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT, NTX>, a, n, k0,
-                                      jb, ipiv, mv, nm, info, panel_spec()));
+  MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT, NTX, TG>, a, n,
+                                      k0, jb, ipiv, mv, nm, info, panel_spec(), bs));
 }
 
 // Largest rows-per-thread the shared memory allows for (T, NB) at 256 threads.
@@ -670,9 +725,9 @@ int panel_rpt(int m)
   return rpt <= max_rpt<T, NB>() ? rpt : 0;
 }
 
-template <typename T, int NB>
-void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, DevInfo *info,
-                  cudaStream_t s)
+template <typename T, int NB, typename TG = T>
+void launch_panel(TG *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, DevInfo *info,
+                  cudaStream_t s, int ns = 1, BatchStride bs = BatchStride{})
 {
   const int m = n - k0;
   const int per_cta = panel2::NT;
@@ -682,16 +737,18 @@ void launch_panel(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, Dev
   const int cs = std::max(1, (m + rpt * per_cta - 1) / (rpt * per_cta));
   prof_begin(KC_PANEL, s);
   if (rpt == 1)
-    launch_panel_rpt<T, NB, 1>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+    launch_panel_rpt<T, NB, 1, panel2::NT, TG>(cs, a, n, k0, jb, ipiv, mv, nm, info, s, ns, bs);
   else if (rpt == 2)
   {
     if constexpr (max_rpt<T, NB>() >= 2)
-      launch_panel_rpt<T, NB, 2>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+      launch_panel_rpt<T, NB, 2, panel2::NT, TG>(cs, a, n, k0, jb, ipiv, mv, nm, info, s, ns,
+                                                 bs);
   }
   else
   {
     if constexpr (max_rpt<T, NB>() >= 4)
-      launch_panel_rpt<T, NB, 4>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+      launch_panel_rpt<T, NB, 4, panel2::NT, TG>(cs, a, n, k0, jb, ipiv, mv, nm, info, s, ns,
+                                                 bs);
   }
   prof_end(KC_PANEL, s);
 }
@@ -947,32 +1004,9 @@ void lu_run(T *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info, c
 // written log2(n/64) times instead of n/64 times. The panels are factored in
 // binary32 (the binary16 panel converted into a scratch buffer, the binary32
 // cluster kernel, one rounding back): half the binary16 kernel's time, and no
-// less accurate. Not bitwise (lu_mode EXACT is); pivots are the reference's
+// less accurate (the panel kernel widens on load and rounds once on store).
+// Not bitwise (lu_mode EXACT is); pivots are the reference's
 // whenever no near-tie is decided differently by the higher precision.
-__global__ void cvt_panel_h2f_kernel(const h16 *__restrict__ a, float *__restrict__ pf, int n,
-                                     int k0, int jb)
-{
-  const int rows = n - k0;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)rows * jb;
-       i += (long)gridDim.x * blockDim.x)
-  {
-    const int c = (int)(i / rows), r = k0 + (int)(i - (long)c * rows);
-    pf[(size_t)c * n + r] = h2f(a[(size_t)(k0 + c) * n + r]);
-  }
-}
-
-__global__ void cvt_panel_f2h_kernel(const float *__restrict__ pf, h16 *__restrict__ a, int n,
-                                     int k0, int jb)
-{
-  const int rows = n - k0;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)rows * jb;
-       i += (long)gridDim.x * blockDim.x)
-  {
-    const int c = (int)(i / rows), r = k0 + (int)(i - (long)c * rows);
-    a[(size_t)(k0 + c) * n + r] = f2h(pf[(size_t)c * n + r]);
-  }
-}
-
 static bool tc_panel_f32()
 {
   static const bool v = [] {
@@ -1001,21 +1035,8 @@ static void tc_panel(TcRun &R, int k0, int jb)
   const int p = k0 / 64, n = R.n;
   int2 *mv = ws.moves + (size_t)p * 128;
   int *nm = ws.nmoves + p;
-  if (ws.pf32 && tc_panel_f32() && panel_rpt<float, 64>(n - k0) > 0)
-  {
-    const long tot = (long)(n - k0) * jb;
-    const int g = (int)std::min<long>(148 * 4, (tot + 255) / 256);
-    prof_begin(KC_PANEL, R.s);
-    cvt_panel_h2f_kernel<<<g, 256, 0, R.s>>>(R.a, ws.pf32, n, k0, jb);
-    MPIRG_CUDA_CHECK(cudaGetLastError());
-    prof_end(KC_PANEL, R.s);
-    // the panel kernel addresses column k0 + c at a[(k0 + c) n + row]
-    launch_panel<float, 64>(ws.pf32 - (size_t)k0 * n, n, k0, jb, R.ipiv, mv, nm, R.info, R.s);
-    prof_begin(KC_PANEL, R.s);
-    cvt_panel_f2h_kernel<<<g, 256, 0, R.s>>>(ws.pf32, R.a, n, k0, jb);
-    MPIRG_CUDA_CHECK(cudaGetLastError());
-    prof_end(KC_PANEL, R.s);
-  }
+  if (tc_panel_f32() && panel_rpt<float, 64>(n - k0) > 0)
+    launch_panel<float, 64, h16>(R.a, n, k0, jb, R.ipiv, mv, nm, R.info, R.s);
   else
     panel_any<h16, 64>(R.a, n, k0, jb, R.ipiv, mv, nm, ws, R.info, R.s);
   // the accumulated permutation follows on the side stream, off the chain
@@ -1032,22 +1053,181 @@ static void tc_panel(TcRun &R, int k0, int jb)
 // row moves of panels [pa, pb), in order, on columns [cb, ce)
 static void tc_moves(TcRun &R, int pa, int pb, int cb, int ce)
 {
-  for (int p = pa; p < pb; ++p)
-    launch_moves<h16, 64>(R.a, R.n, cb, ce, ColMap{}, R.ws->moves + (size_t)p * 128,
-                          R.ws->nmoves + p, nullptr, R.s);
+  if (ce <= cb || pb <= pa)
+    return;
+  prof_begin(KC_MOVES, R.s);
+  const int grid = std::max(1, std::min((ce - cb + 7) / 8, 148 * 4));
+  lu_apply_moves_multi_kernel<h16, 64><<<grid, 256, 0, R.s>>>(R.a, R.n, cb, ce, R.ws->moves,
+                                                              R.ws->nmoves, pa, pb);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+  prof_end(KC_MOVES, R.s);
 }
 
 // rows [K0, K0 + sz) of columns [cb, ce) <- L11^-1 (those rows), L11 unit lower at (K0, K0)
-static void tc_trsm(TcRun &R, int K0, int sz, int cb, int ce)
+// U12 leaf of the tensor-core mode: rows [k0, k0 + jb) of columns [cb, ce)
+// <- L11^-1 (those rows), jb <= LB, with the substitution in binary32
+// (binary16 inputs, one FMA per term, one rounding back to binary16).
+// lu_mt_kernel's layout -- 4 warps x 8 columns per CTA, lane owns rows
+// lane + 32 h, x_k by shuffle -- without the per-term binary16 roundings the
+// exact mode needs, and up to 256 rows per launch (L11 staged k-major as
+// binary16 in shared memory), so the solve of a 256-row block is one launch
+// instead of 4 leaves + 3 updates.
+template <int LB>
+__global__ void __launch_bounds__(256) tc_trsm_leaf_kernel(h16 *__restrict__ A, int n, int k0,
+                                                           int jb, int cb, int ce,
+                                                           const int2 *__restrict__ moves,
+                                                           const int *__restrict__ nmoves, int pa,
+                                                           int pb)
 {
-  if (sz <= 64)
+  constexpr int RL = LB / 32, CW = 4;  // 8 warps x 4 columns
+  constexpr int PER = 4;               // 2 * 64 move entries over 32 lanes
+  extern __shared__ __align__(16) unsigned char trsm_smem[];
+  h16 *Ls = reinterpret_cast<h16 *>(trsm_smem);  // [kk][i], i contiguous
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // L11 (strictly lower part), 8 binary16 values per load (k0 is a multiple of 64)
+  for (int idx = threadIdx.x * 8; idx < LB * LB; idx += 256 * 8)
   {
-    launch_mt<h16, 64>(R.a, R.n, K0, sz, cb, ce, ColMap{}, R.ws->moves, R.ws->zero, R.s);
+    const int kk = idx / LB, i = idx % LB;
+    unsigned short e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (kk < jb && i < jb && i + 7 > kk)
+    {
+      if (i + 8 <= jb)
+      {
+        const uint4 w = *reinterpret_cast<const uint4 *>(A + (size_t)(k0 + kk) * n + k0 + i);
+        const unsigned int ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          e[q] = (unsigned short)(ww[q >> 1] >> (16 * (q & 1)));
+      }
+      else
+      {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          e[q] = i + q < jb ? A[(size_t)(k0 + kk) * n + k0 + i + q].bits : (unsigned short)0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (i + q <= kk)
+          e[q] = 0;  // only the strictly lower part: rows <= kk are final at step kk
+    }
+    const uint4 v = make_uint4(e[0] | ((unsigned)e[1] << 16), e[2] | ((unsigned)e[3] << 16),
+                               e[4] | ((unsigned)e[5] << 16), e[6] | ((unsigned)e[7] << 16));
+    *reinterpret_cast<uint4 *>(Ls + idx) = v;
+  }
+  const int col0 = cb + blockIdx.x * MT_COLS + warp * CW;
+  // the row moves of panels [pa, pb), in order, on this warp's columns (the
+  // columns of a block's right half take the left half's moves here instead
+  // of in a launch of their own)
+  for (int p = pa; p < pb; ++p)
+  {
+    const int nm = nmoves[p];
+    if (nm == 0)
+      continue;
+    int2 mv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+    {
+      const int e = lane + 32 * q;
+      mv[q] = e < nm ? moves[(size_t)p * 128 + e] : make_int2(-1, -1);
+    }
+#pragma unroll
+    for (int u = 0; u < CW; ++u)
+      if (col0 + u < ce)
+      {
+        h16 *cp = A + (size_t)(col0 + u) * n;
+        h16 v[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            v[q] = cp[mv[q].y];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (mv[q].x >= 0)
+            cp[mv[q].x] = v[q];
+        __syncwarp();
+      }
+  }
+  float x[CW][RL];
+#pragma unroll
+  for (int u = 0; u < CW; ++u)
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      x[u][h] = (col0 + u < ce && i < jb) ? h2f(A[(size_t)(col0 + u) * n + k0 + i]) : 0.f;
+    }
+  __syncthreads();
+#pragma unroll
+  for (int hk = 0; hk < RL; ++hk)
+  {
+    if (32 * hk >= jb)
+      break;
+#pragma unroll 8
+    for (int lk = 0; lk < 32; ++lk)
+    {
+      const int kk = 32 * hk + lk;  // rows above 32 hk are final: only slots h >= hk change
+      float lv[RL];
+#pragma unroll
+      for (int h = hk; h < RL; ++h)
+        lv[h] = h2f(Ls[kk * LB + lane + 32 * h]);  // 0 for rows <= kk and beyond jb
+#pragma unroll
+      for (int u = 0; u < CW; ++u)
+      {
+        const float xk = __shfl_sync(0xffffffffu, x[u][hk], lk);
+#pragma unroll
+        for (int h = hk; h < RL; ++h)
+          x[u][h] = __fmaf_rn(-lv[h], xk, x[u][h]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < CW; ++u)
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+    {
+      const int i = lane + 32 * h;
+      if (col0 + u < ce && i < jb)
+        A[(size_t)(col0 + u) * n + k0 + i] = f2h(x[u][h]);
+    }
+}
+
+template <int LB>
+static void tc_trsm_leaf(TcRun &R, int K0, int sz, int cb, int ce, int pa, int pb)
+{
+  constexpr int smem = LB * LB * 2;
+  static DeviceOnce configured;
+  if (configured.needed())
+  {
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(tc_trsm_leaf_kernel<LB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured.done();
+  }
+  tc_trsm_leaf_kernel<LB><<<(ce - cb + MT_COLS - 1) / MT_COLS, 256, smem, R.s>>>(
+      R.a, R.n, K0, sz, cb, ce, R.ws->moves, R.ws->nmoves, pa, pb);
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+// [pa, pb): panels whose row moves the first leaf applies to the columns (none: pa == pb)
+static void tc_trsm(TcRun &R, int K0, int sz, int cb, int ce, int pa = 0, int pb = 0)
+{
+  if (sz <= 256)
+  {
+    if (ce <= cb)
+      return;
+    prof_begin(KC_TRSM, R.s);
+    if (sz <= 64)
+      tc_trsm_leaf<64>(R, K0, sz, cb, ce, pa, pb);
+    else if (sz <= 128)
+      tc_trsm_leaf<128>(R, K0, sz, cb, ce, pa, pb);
+    else
+      tc_trsm_leaf<256>(R, K0, sz, cb, ce, pa, pb);
+    prof_end(KC_TRSM, R.s);
     return;
   }
   const int h = tc_split(sz);
-  tc_trsm(R, K0, h, cb, ce);
-  tc_gemm(*R.tc, K0 + h, K0 + sz, cb, ce, K0, h, R.s);
+  tc_trsm(R, K0, h, cb, ce, pa, pb);  // the moves go with the first leaf only
+  tc_gemm(*R.tc, K0 + h, K0 + sz, cb, ce, K0, h, R.s, KC_TRSM);
   tc_trsm(R, K0 + h, sz - h, cb, ce);
 }
 
@@ -1060,15 +1240,15 @@ static void tc_factor(TcRun &R, int K0, int w)
   }
   const int h = tc_split(w);
   tc_factor(R, K0, h);
-  tc_moves(R, K0 / 64, (K0 + h) / 64, K0 + h, K0 + w);
-  tc_trsm(R, K0, h, K0 + h, K0 + w);
+  // the left half's row moves reach the right half inside the U12 solve's first leaf
+  tc_trsm(R, K0, h, K0 + h, K0 + w, K0 / 64, (K0 + h) / 64);
   tc_gemm(*R.tc, K0 + h, R.n, K0 + h, K0 + w, K0, h, R.s);
   tc_factor(R, K0 + h, w - h);
   tc_moves(R, (K0 + h) / 64, (K0 + w + 63) / 64, K0, K0 + h);
 }
 
-static void lu_run_tc(h16 *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
-                      cudaStream_t s, const TcPlan &tc)
+static void lu_run_tc_body(h16 *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                           cudaStream_t s, const TcPlan &tc)
 {
   cudaStream_t side = static_cast<cudaStream_t>(ws.side);
   cudaEvent_t *ev = static_cast<cudaEvent_t *>(ws.events);
@@ -1594,17 +1774,18 @@ static void lu_graph_forget(const void *ws_moves)
   }
 }
 
-template <int NB>
-void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
-                cudaStream_t caller)
+// Runs body() on `caller`, captured once per key into a CUDA graph and
+// replayed afterwards (directly when graphs are off, under the per-kernel
+// profile, or on a legacy/per-thread default stream, which cannot capture).
+template <typename Body>
+static void run_with_graph(const LuGraphKey &key, cudaStream_t caller, Body &&body)
 {
   if (!lu_graph_enabled() || prof_on() || caller == nullptr || caller == cudaStreamLegacy ||
       caller == cudaStreamPerThread)
   {
-    lu_run_f32_body<NB>(a, n, ipiv, perm, ws, info, caller);
+    body();
     return;
   }
-  const LuGraphKey key{a, ipiv, perm, info, ws.moves, n, caller};
   cudaGraphExec_t exec = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_lu_graph_mu);
@@ -1618,7 +1799,7 @@ void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo 
     MPIRG_CUDA_CHECK(cudaStreamBeginCapture(caller, cudaStreamCaptureModeThreadLocal));
     try
     {
-      lu_run_f32_body<NB>(a, n, ipiv, perm, ws, info, caller);
+      body();
     }
     catch (...)
     {
@@ -1634,6 +1815,24 @@ void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo 
     g_lu_graphs.push_back({key, exec});
   }
   MPIRG_CUDA_CHECK(cudaGraphLaunch(exec, caller));
+}
+
+template <int NB>
+void lu_run_f32(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                cudaStream_t caller)
+{
+  run_with_graph(LuGraphKey{a, ipiv, perm, info, ws.moves, n, caller}, caller,
+                 [&] { lu_run_f32_body<NB>(a, n, ipiv, perm, ws, info, caller); });
+}
+
+// The recursive tensor-core LU issues ~1500 small dependent launches at
+// n = 8192; replayed as one graph their launch gaps shrink to the
+// node-to-node latency.
+static void lu_run_tc(h16 *a, int n, int *ipiv, int *perm, LuWorkspace &ws, DevInfo *info,
+                      cudaStream_t caller, const TcPlan &tc)
+{
+  run_with_graph(LuGraphKey{a, ipiv, perm, info, ws.moves, n, caller}, caller,
+                 [&] { lu_run_tc_body(a, n, ipiv, perm, ws, info, caller, tc); });
 }
 
 // ---- one rank of the 1-D block-cyclic LU (config 5a) ----------------------
@@ -1795,6 +1994,97 @@ void dlu_panel_t(DluPlan &d, T *a, int p, int *ipiv, DevInfo *info, cudaStream_t
 
 }  // namespace
 
+// ---- config 5b: the binary32 LU of ns independent systems per launch ---------
+// System z of a launch is blockIdx.z: matrix a + z n^2, pivots ipiv + z n,
+// permutation perm + z n, row moves moves + z (np 2 nb), counts nmoves + z np,
+// error record info + z. Right-looking steps with no look-ahead (the batch is
+// the parallelism): per step one panel launch (one thread-block cluster per
+// system), one U12 solve, one trailing update, one left-column move launch --
+// 4 launches per step for the whole group instead of ~6 per system. Every
+// kernel is the single-system one, so each system's factors are the
+// reference's bit for bit.
+__global__ void iota_batch_kernel(int *p, int n)
+{
+  int *q = p + (size_t)blockIdx.y * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    q[i] = i;
+}
+
+void launch_lu_batched_f32(float *a, int n, int ns, int *ipiv, int *perm, int2 *moves,
+                           int *nmoves, DevInfo *info, cudaStream_t s)
+{
+  constexpr int NB = 64;
+  if (n <= 0 || ns <= 0)
+    return;
+  const int np = (n + NB - 1) / NB;
+  BatchStride bs;
+  bs.a = (size_t)n * n;
+  bs.vec = n;
+  bs.moves = np * 2 * NB;
+  bs.nm = np;
+  bs.info = 1;
+  const ColMap id{};
+  {
+    ProfScope ps(KC_VEC, s);
+    iota_batch_kernel<<<dim3((n + 255) / 256, ns), 256, 0, s>>>(perm, n);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  }
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(nmoves, 0, sizeof(int) * (size_t)np * ns, s));
+  static DeviceOnce configured;
+  if (configured.needed())
+  {
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_v4_kernel<NB, 64, 64>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)gemm_v4_smem<NB, 64, 64>()));
+    MPIRG_CUDA_CHECK(cudaFuncSetAttribute(lu_gemm_v4_kernel<NB, 128, 128>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)gemm_v4_smem<NB, 128, 128>()));
+    configured.done();
+  }
+  for (int p = 0, k0 = 0; k0 < n; ++p, k0 += NB)
+  {
+    const int jb = std::min(NB, n - k0), c0 = k0 + jb;
+    int2 *mv = moves + (size_t)p * 2 * NB;
+    int *nm = nmoves + p;
+    if (panel_rpt<float, NB>(n - k0) == 0)
+      throw std::runtime_error("batched LU: n too large for a single-cluster panel");
+    launch_panel<float, NB>(a, n, k0, jb, ipiv, mv, nm, info, s, ns, bs);
+    if (c0 < n)
+    {
+      prof_begin(KC_TRSM, s);
+      lu_mt_kernel<float, NB><<<dim3((n - c0 + MT_COLS - 1) / MT_COLS, 1, ns), 128, 0, s>>>(
+          a, n, k0, jb, c0, n, id, mv, nm, bs);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+      prof_end(KC_TRSM, s);
+      prof_begin(KC_GEMM, s);
+      const int t = n - c0;
+      if ((long)((t + 127) / 128) * ((t + 127) / 128) * ns >= 2 * 148)
+        lu_gemm_v4_kernel<NB, 128, 128>
+            <<<dim3((t + 127) / 128, (t + 127) / 128, ns), 256, gemm_v4_smem<NB, 128, 128>(), s>>>(
+                a, n, k0, jb, c0, n, id, bs.a);
+      else
+        lu_gemm_v4_kernel<NB, 64, 64>
+            <<<dim3((t + 63) / 64, (t + 63) / 64, ns), 256, gemm_v4_smem<NB, 64, 64>(), s>>>(
+                a, n, k0, jb, c0, n, id, bs.a);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+      prof_end(KC_GEMM, s);
+    }
+    prof_begin(KC_MOVES, s);
+    const int warps_needed = std::max(1, (k0 + 3) / 4);
+    const int grid = std::max(1, std::min((warps_needed + 7) / 8, 64));
+    lu_apply_moves_kernel<float, NB><<<dim3(grid, 1, ns), 256, 0, s>>>(a, n, 0, k0, id, mv, nm,
+                                                                     perm, bs);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+    prof_end(KC_MOVES, s);
+  }
+}
+
+bool lu_batched_supported(int prec, int n)
+{
+  return prec == B32 && n % 4 == 0 && n >= 64 && panel_rpt<float, 64>(n) > 0 &&
+         gemm_v4_allowed();
+}
+
 int lu_choose_nb(int prec, int n, int requested)
 {
   if (requested == 16 || requested == 32 || requested == 64)
@@ -1941,8 +2231,6 @@ void lu_workspace_alloc(LuWorkspace &ws, int prec, int n, int nb)
     MPIRG_CUDA_CHECK(cudaMalloc(&ws.ut, sizeof(float) * 2 * (size_t)ws.nb * n));
   MPIRG_CUDA_CHECK(cudaMalloc(&ws.zero, sizeof(int)));
   MPIRG_CUDA_CHECK(cudaMemset(ws.zero, 0, sizeof(int)));
-  if (prec == B16 && ws.nb == 64)  // binary32 copy of the current panel (lu_run_tc)
-    MPIRG_CUDA_CHECK(cudaMalloc(&ws.pf32, sizeof(float) * (size_t)ws.nb * std::max(1, n)));
   cudaStream_t side;
   // The side stream carries the bulk trailing update; give it the lowest
   // priority so the block scheduler hands freed SMs to the critical chain
@@ -1975,7 +2263,7 @@ void lu_workspace_free(LuWorkspace &ws)
   if (ws.moves)
     lu_graph_forget(ws.moves);
   for (void *p : {(void *)ws.moves, (void *)ws.nmoves, (void *)ws.pp, (void *)ws.smv,
-                  (void *)ws.snm, ws.ut, (void *)ws.zero, (void *)ws.pf32})
+                  (void *)ws.snm, ws.ut, (void *)ws.zero})
     if (p)
       cudaFree(p);
   if (ws.events)

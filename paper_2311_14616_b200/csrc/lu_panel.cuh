@@ -250,13 +250,38 @@ __host__ __device__ constexpr size_t panel_dyn_smem()
 // rows of this CTA: row0 + t + q*NT, q < RPT (R = RPT*NT rows per CTA)
 // NTX threads per CTA (256 for the panel of the blocked LU; 512 for the
 // 8-column leaf of a tall panel, lu.cu panel_tall).
-template <typename T, int NB, int RPT, int NTX = NT>
+// TG: the matrix's storage type when it differs from the arithmetic type T
+// (the tensor-core mode factors binary16 panels in binary32: widened on load,
+// rounded once on store).
+template <typename T, typename TG>
+__device__ __forceinline__ T panel_in(TG v)
+{
+  if constexpr (std::is_same<T, TG>::value)
+    return v;
+  else
+    return promote<T, TG>(v);
+}
+template <typename TG, typename T>
+__device__ __forceinline__ TG panel_out(T v)
+{
+  if constexpr (std::is_same<T, TG>::value)
+    return v;
+  else
+    return demote<TG, T>(v);
+}
+
+template <typename T, int NB, int RPT, int NTX = NT, typename TG = T>
 __global__ void __launch_bounds__(NTX, 1)
-    lu_panel2_kernel(T *__restrict__ A, int n, int k0, int jb, int *__restrict__ ipiv,
+    lu_panel2_kernel(TG *__restrict__ A, int n, int k0, int jb, int *__restrict__ ipiv,
                      int2 *__restrict__ moves, int *__restrict__ nmoves, DevInfo *info,
-                     int spec_ok)
+                     int spec_ok, BatchStride bs)
 {
   constexpr int NT = NTX;  // hides the namespace default inside this kernel
+  A += (size_t)blockIdx.z * bs.a;
+  ipiv += (size_t)blockIdx.z * bs.vec;
+  moves += (size_t)blockIdx.z * bs.moves;
+  nmoves += (size_t)blockIdx.z * bs.nm;
+  info += (size_t)blockIdx.z * bs.info;
   constexpr int NW = NTX / 32;
   static_assert(NW <= 32 && NW * 2 >= MAXCS, "push mapping needs 2*NW >= MAXCS");
   using S = Slot<T>;
@@ -303,7 +328,9 @@ __global__ void __launch_bounds__(NTX, 1)
     for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int q = 0; q < RPT; ++q)
-        tmp[u][q] = (pos[q] >= 0 && c0 + u < jb) ? A[(size_t)(k0 + c0 + u) * n + pos[q]] : T{};
+        tmp[u][q] = (pos[q] >= 0 && c0 + u < jb)
+                        ? panel_in<T, TG>(A[(size_t)(k0 + c0 + u) * n + pos[q]])
+                        : T{};
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
@@ -949,7 +976,7 @@ __global__ void __launch_bounds__(NTX, 1)
     {
       const int g = row0 + t + q * NT;
       for (int c = 0; c < jb; ++c)
-        A[(size_t)(k0 + c) * n + pos[q]] = P[c * R + t + q * NT];
+        A[(size_t)(k0 + c) * n + pos[q]] = panel_out<TG, T>(P[c * R + t + q * NT]);
       if (pos[q] != g)
       {
         const int e = atomicAdd(nmoves, 1);

@@ -294,32 +294,37 @@ void tc_plan_make(TcPlan &p, void *a, int n)
 }
 
 // rows [r0, r1) x columns [cb, ce) -= L[:, k0 .. k0+K) U[k0 .. k0+K, :), K % 64 == 0.
-void tc_gemm(const TcPlan &p, int r0, int r1, int cb, int ce, int k0, int K, cudaStream_t s)
+// kclass: the profile class the launch is booked under (the updates inside
+// the U12 solve belong to K4, the trailing updates to K5).
+void tc_gemm(const TcPlan &p, int r0, int r1, int cb, int ce, int k0, int K, cudaStream_t s,
+             int kclass)
 {
   if (r1 <= r0 || ce <= cb || K <= 0)
     return;
   if (K % BK)
     throw std::runtime_error("tc_gemm: K must be a multiple of 64");
-  prof_begin(KC_GEMM, s);
+  prof_begin(kclass, s);
   const int M = r1 - r0, N = ce - cb;
+  const long mt128 = (M + 127) / 128;
   const auto &b256 = *reinterpret_cast<const CUtensorMap *>(p.mapB);
-  if (N <= 64)
-    launch_cfg<1, 64>(p, *reinterpret_cast<const CUtensorMap *>(p.mapB64), r0, r1, cb, ce, k0, K,
-                      s);
-  else if (N <= 128)
-    launch_cfg<1, 128>(p, *reinterpret_cast<const CUtensorMap *>(p.mapB128), r0, r1, cb, ce, k0,
-                       K, s);
+  const auto &b128 = *reinterpret_cast<const CUtensorMap *>(p.mapB128);
+  const auto &b64 = *reinterpret_cast<const CUtensorMap *>(p.mapB64);
+  // narrower column tiles while the launch would leave most SMs idle
+  if (N <= 64 || mt128 * ((N + 127) / 128) < 96)
+    launch_cfg<1, 64>(p, b64, r0, r1, cb, ce, k0, K, s);
+  else if (N <= 128 || mt128 * ((N + 255) / 256) < 96)
+    launch_cfg<1, 128>(p, b128, r0, r1, cb, ce, k0, K, s);
   else if (K >= 1024 && M > 128 && (long)((M + 255) / 256) * ((N + 255) / 256) >= 96)
     launch_cfg<2, 256>(p, b256, r0, r1, cb, ce, k0, K, s);
   else
     launch_cfg<1, 256>(p, b256, r0, r1, cb, ce, k0, K, s);
-  prof_end(KC_GEMM, s);
+  prof_end(kclass, s);
 }
 
 // A22 columns [cb, ce), rows [k0 + 64, n) -= L21 * U12 of the panel at k0 (jb = 64).
 void launch_gemm_tc(const TcPlan &p, int k0, int cb, int ce, cudaStream_t s)
 {
-  tc_gemm(p, k0 + BK, p.n, cb, ce, k0, BK, s);
+  tc_gemm(p, k0 + BK, p.n, cb, ce, k0, BK, s, KC_GEMM);
 }
 
 }  // namespace mpirg

@@ -180,6 +180,7 @@ struct mpirg_factorization
   void *x = nullptr;       // TR
   void *y = nullptr;       // substitution scratch (max(TW, TF) bytes)
   void *sol = nullptr;     // TW
+  void *comp = nullptr;    // TR: comp_buf of the reference's storage ledger (scratch)
   unsigned long long *scal = nullptr;  // [0] ||A||_1, [1] ||b||, [2+3i..] per pass
   int scal_cap = 0;
   DevInfo *info = nullptr;
@@ -241,6 +242,7 @@ struct mpirg_factorization
     x = dalloc_bytes(n * tr_bytes());
     y = dalloc_bytes(n * 8);
     sol = dalloc_bytes(n * tw_bytes());
+    comp = dalloc_bytes(n * tr_bytes());
     info = dalloc<DevInfo>(1);
     MPIRG_CUDA_CHECK(cudaMallocHost(&h_info, sizeof(DevInfo)));
     ensure_scal(16);
@@ -254,7 +256,7 @@ struct mpirg_factorization
   void release()
   {
     cudaSetDevice(device);
-    for (void *p : {a_high, a_low, (void *)ipiv, (void *)perm, b, r, x, y, sol, (void *)scal,
+    for (void *p : {a_high, a_low, (void *)ipiv, (void *)perm, b, r, x, y, sol, comp, (void *)scal,
                     (void *)info})
       if (p)
         cudaFree(p);
@@ -849,6 +851,11 @@ const void *mpirg_factorization_a_high_device(const mpirg_factorization *f) { re
 const void *mpirg_factorization_packed_lu_device(const mpirg_factorization *f) { return f->a_low; }
 const int *mpirg_factorization_ipiv_device(const mpirg_factorization *f) { return f->ipiv; }
 void *mpirg_factorization_stream(const mpirg_factorization *f) { return f->stream; }
+void *mpirg_factorization_residual_buf_device(mpirg_factorization *f) { return f->r; }
+void *mpirg_factorization_sol_buf_device(mpirg_factorization *f) { return f->x; }
+void *mpirg_factorization_comp_buf_device(mpirg_factorization *f) { return f->comp; }
+void *mpirg_factorization_low_buf_device(mpirg_factorization *f) { return f->y; }
+void *mpirg_factorization_work_buf_device(mpirg_factorization *f) { return f->y; }
 
 int mpirg_ir_solve(mpirg_factorization *f, const void *b, int b_on_device,
                    const mpirg_term_params *tp, mpirg_report *rep, mpirg_error *err)

@@ -6,9 +6,10 @@ rounding per panel step instead of two roundings per term), so:
   the same operation, fp16(fp32(C) - L21 U12): within 1 binary16 ulp
   everywhere and exact on >= 99% of the tile (fp32 accumulation order is the
   tensor core's); untouched regions stay bit-identical;
-* solve level (config 3 shape): the refined solution within the bound
-  SURVEY.md 8(d) derives from the stopping rule, 2*kappa*ce*eps32*
-  (||b|| + ||A||_1 ||x||)/||x||, against the exact (reference-bitwise) path.
+* solve level (config 3 shape): the refined solution within BASELINE's
+  tolerance 10*eps32*||x||_inf of the exact (reference-bitwise) path, and within
+  the (looser) bound SURVEY.md 8(d) derives from the stopping rule,
+  2*kappa*ce*eps32*(||b|| + ||A||_1 ||x||)/||x||.
 """
 import ctypes as C
 
@@ -145,3 +146,8 @@ def test_tc_mode_solution_within_stopping_rule_bound(gpulib, n):
         np.abs(xe))
     rel = np.max(np.abs(tc["x"] - xe)) / np.max(np.abs(xe))
     assert rel <= bound, (rel, bound)
+    # BASELINE.json's own tolerance for config 3, 10 eps32 ||x||_inf: met by the
+    # recursive tensor-core LU at every size measured (profiles/r02*_tc_deviation:
+    # 8.4e-7 at n = 1024, 2.1e-7 at n = 8192); the stopping rule admits up to
+    # `bound`, so this is asserted where it was measured, not promised in general
+    assert rel <= 10 * eps32, (rel, 10 * eps32)
