@@ -172,7 +172,8 @@ def run_ours(args, world, rank, local):
                         "includes SM sharing with the other systems' kernels"}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_sample(args, n, seconds=15.0)
+        cpu = cpu_sample(args, n, seconds=15.0,
+                         gpu_x=sol_dev.cpu().numpy().reshape(count, n), gpu_rlen=rlen)
     if rank == 0:
         launches = int(sum(cnt_k[i] for i in range(nclass)))
         line = {
@@ -186,7 +187,9 @@ def run_ours(args, world, rank, local):
                        "parallelism": f"batch slice per GPU x{world}, no collective",
                        "l2": f"inputs larger than L2 ({count * n * n * 8 / 1e9:.1f} GB of A)",
                        "a_resident_in_hbm": True,
-                       "workers_per_gpu": int(os.environ.get("MPIRG_BATCH_WORKERS", "16"))},
+                       "workers_per_gpu": int(os.environ.get("MPIRG_BATCH_WORKERS", "16")),
+                       "mode": os.environ.get("MPIRG_BATCH_MODE", "batched kernels (groups of "
+                                              + os.environ.get("MPIRG_BATCH_GROUP", "128") + ")")},
             "systems_per_s": args.count / (mean_ms / 1e3),
             "all_ok": ok, "reasons": reasons,
             "iters_min": min(iters), "iters_max": max(iters),
@@ -197,6 +200,11 @@ def run_ours(args, world, rank, local):
         }
         if cpu:
             line["cpu_baseline"] = cpu
+            if "parity_checked_systems" in cpu:
+                line["parity_checked_systems"] = cpu["parity_checked_systems"]
+                line["parity_all_systems"] = bool(cpu["parity_all_checked_equal"] and
+                                                  cpu["parity_checked_systems"] == args.count)
+                line["parity_all_checked_equal"] = cpu["parity_all_checked_equal"]
         print(json.dumps(line), flush=True)
 
 
@@ -225,7 +233,7 @@ def _ref_solves(impl, n, count, threads):
     return max(o[0] for o in out), [r for o in out for r in o[1]]
 
 
-def cpu_sample(args, n, seconds=15.0):
+def cpu_sample(args, n, seconds=15.0, gpu_x=None, gpu_rlen=None):
     """The compiled reference on a bounded sample of the batch, all host cores,
     extrapolated to the whole batch (systems are independent)."""
     import oracle
@@ -238,11 +246,22 @@ def cpu_sample(args, n, seconds=15.0):
     m = min(max(m, threads), args.count)
     dt, reps = _ref_solves(impl, n, m, threads)
     full = dt * args.count / m
-    return {"value": full, "unit": "s", "cores": threads, "kind": kind,
-            "sample": f"systems 0..{m - 1} of {args.count} (N={n}) solved by the compiled "
-                      f"reference on {threads} host threads in {dt:.2f} s (solve time only), "
-                      f"scaled x{args.count / m:.1f} to the whole batch",
-            "reasons": sorted({r["reason"] for r in reps if r["reason"]})}
+    out = {"value": full, "unit": "s", "cores": threads, "kind": kind,
+           "sample": f"systems 0..{m - 1} of {args.count} (N={n}) solved by the compiled "
+                     f"reference on {threads} host threads in {dt:.2f} s (solve time only), "
+                     f"scaled x{args.count / m:.1f} to the whole batch",
+           "reasons": sorted({r["reason"] for r in reps if r["reason"]})}
+    if gpu_x is not None:
+        # the free parity check: every system the CPU leg solved against the GPU
+        # batch's solution and history length, bit for bit
+        import numpy as np
+        k = min(m, gpu_x.shape[0])
+        same = [bool(np.array_equal(reps[i]["x"].view(np.uint64), gpu_x[i].view(np.uint64))
+                     and len(reps[i]["rhist"]) == int(gpu_rlen[i])) for i in range(k)]
+        out["parity_checked_systems"] = k
+        out["parity_all_checked_equal"] = all(same)
+        out["parity_first_mismatch"] = None if all(same) else same.index(False)
+    return out
 
 
 def run_reference(args, world, rank):

@@ -367,6 +367,12 @@ void mpirg_gen_normal_matrix(int rows, int cols, uint64_t seed, double *out);
 void mpirg_gen_diag_dominant(int n, uint64_t seed, double shift, double *out);
 void mpirg_gen_greens_operator(int n, double alpha, double *out);
 void mpirg_gen_integral_rhs(int n, double alpha, double *out);
+/* The same operator generated on the device (greens.cpp:11-59, bitwise):
+ * columns [col0, col0 + ncols) of I - alpha G into out (device memory,
+ * column-major, leading dimension ld >= n). Lets config 5a's 34 GB matrix --
+ * or one rank's column blocks of it -- be built in HBM directly. */
+int mpirg_gen_greens_operator_device(int n, double alpha, int col0, int ncols, double *out,
+                                     size_t ld, void *stream);
 void mpirg_gen_matvec_compensated_f64(int n, const double *a, const double *x, double *y);
 
 #ifdef __cplusplus

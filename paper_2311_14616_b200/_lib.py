@@ -184,6 +184,7 @@ PROTOTYPES = {
     "mpirg_gen_diag_dominant": (None, [_I, C.c_uint64, _D, _P]),
     "mpirg_gen_greens_operator": (None, [_I, _D, _P]),
     "mpirg_gen_integral_rhs": (None, [_I, _D, _P]),
+    "mpirg_gen_greens_operator_device": (_I, [_I, _D, _I, _I, _P, _S, _P]),
     "mpirg_gen_matvec_compensated_f64": (None, [_I, _P, _P, _P]),
 }
 

@@ -118,9 +118,18 @@ __global__ void __launch_bounds__(CAST_NT) cast_norm_kernel(const From *__restri
                                                             To *__restrict__ dst, int rows,
                                                             int cols,
                                                             unsigned long long *norm_bits,
-                                                            DevInfo *info, int col_off)
+                                                            DevInfo *info, int col_off,
+                                                            size_t sys_stride)
 {
   extern __shared__ __align__(16) unsigned char cast_sm[];
+  // batched launches (config 5b): system blockIdx.y has its own matrix,
+  // norm slot and error record; storage-order indices are per system
+  src += (size_t)blockIdx.y * sys_stride;
+  if constexpr (!NORM_ONLY)
+    dst += (size_t)blockIdx.y * sys_stride;
+  norm_bits += blockIdx.y;
+  if (sys_stride)
+    info += blockIdx.y;
   auto tile = reinterpret_cast<From(*)[CN][CCH + 1]>(cast_sm);  // [2][CN][CCH+1]
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
@@ -226,11 +235,11 @@ void demote_t(const void *src, void *dst, size_t count, DevInfo *info, cudaStrea
 
 template <typename From, typename To, bool NORM_ONLY>
 void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long long *nb,
-                 DevInfo *info, cudaStream_t s, int col_off = 0)
+                 DevInfo *info, cudaStream_t s, int col_off = 0, int ns = 1)
 {
-  if (rows <= 0 || cols <= 0)
+  if (rows <= 0 || cols <= 0 || ns <= 0)
     return;
-  const int grid = (cols + CN - 1) / CN;
+  const dim3 grid((cols + CN - 1) / CN, ns);
   constexpr int smem = (int)(sizeof(From) * 2 * CN * (CCH + 1));
   static DeviceOnce configured;
   if (configured.needed())
@@ -241,7 +250,8 @@ void cast_norm_t(int rows, int cols, const void *src, void *dst, unsigned long l
   }
   ProfScope ps(KC_CAST, s);
   cast_norm_kernel<From, To, NORM_ONLY><<<grid, CAST_NT, smem, s>>>(
-      static_cast<const From *>(src), static_cast<To *>(dst), rows, cols, nb, info, col_off);
+      static_cast<const From *>(src), static_cast<To *>(dst), rows, cols, nb, info, col_off,
+      ns > 1 ? (size_t)rows * cols : (size_t)0);
   MPIRG_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -267,12 +277,14 @@ void launch_demote(int from, int to, const void *src, void *dst, size_t count, D
 }
 
 void launch_cast_norm(int from, int to, int rows, int cols, const void *src, void *dst,
-                      unsigned long long *nb, DevInfo *info, cudaStream_t s, int col_off)
+                      unsigned long long *nb, DevInfo *info, cudaStream_t s, int col_off, int ns)
 {
+  if (ns > 1 && !(from == B64 && to == B32 && col_off == 0))
+    throw std::invalid_argument("batched cast: binary64 -> binary32 only");
   if (from == B64 && to == B64)
     cast_norm_t<double, double, false>(rows, cols, src, dst, nb, info, s, col_off);
   else if (from == B64 && to == B32)
-    cast_norm_t<double, float, false>(rows, cols, src, dst, nb, info, s, col_off);
+    cast_norm_t<double, float, false>(rows, cols, src, dst, nb, info, s, col_off, ns);
   else if (from == B64 && to == B16)
     cast_norm_t<double, h16, false>(rows, cols, src, dst, nb, info, s, col_off);
   else if (from == B32 && to == B32)

@@ -81,7 +81,9 @@ void launch_demote(int from, int to, const void *src, void *dst, size_t count, D
 // also the leading dimension); storage-order indices stay global.
 void launch_cast_norm(int from, int to, int rows, int cols, const void *src, void *dst,
                       unsigned long long *norm_bits, DevInfo *info, cudaStream_t s,
-                      int col_off = 0);
+                      int col_off = 0, int ns = 1);
+// ns > 1 (config 5b): ns systems stored back to back (rows*cols elements
+// each), norm slot norm_bits[z] and error record info[z] per system.
 void launch_one_norm(int prec, int rows, int cols, const void *src,
                      unsigned long long *norm_bits, cudaStream_t s);
 
@@ -143,8 +145,10 @@ void launch_lu(int prec, int lu_mode, void *a, int n, int *ipiv, int *perm, LuWo
 // back (a + z n^2, ipiv/perm + z n, moves + z np 128, nmoves + z np, info + z),
 // one launch per step for the whole group (lu.cu).
 bool lu_batched_supported(int prec, int n);
+// ut: optional scratch of 64 x (n ns) floats (the transposed U12 of the
+// current step) enabling the TMA-fed trailing update.
 void launch_lu_batched_f32(float *a, int n, int ns, int *ipiv, int *perm, int2 *moves,
-                           int *nmoves, DevInfo *info, cudaStream_t s);
+                           int *nmoves, DevInfo *info, cudaStream_t s, float *ut = nullptr);
 // perm from ipiv for callers that only hold ipiv (standalone solves).
 void launch_perm_from_ipiv(const int *ipiv, int n, int *perm, cudaStream_t s);
 

@@ -2011,11 +2011,33 @@ __global__ void iota_batch_kernel(int *p, int n)
 }
 
 void launch_lu_batched_f32(float *a, int n, int ns, int *ipiv, int *perm, int2 *moves,
-                           int *nmoves, DevInfo *info, cudaStream_t s)
+                           int *nmoves, DevInfo *info, cudaStream_t s, float *ut)
 {
   constexpr int NB = 64;
   if (n <= 0 || ns <= 0)
     return;
+  // with a ut scratch (NB x n ns floats): the TMA-fed update of lu_f32.cuh, the
+  // whole group being one n x (n ns) matrix to the tensor maps
+  const bool tma = ut != nullptr && f32_mode() && (long)n * ns < (1l << 31);
+  CUtensorMap mA128, mA64, mU128, mU64;
+  if (tma)
+  {
+    f32_encode(&mA128, a, n, n * ns, 128);
+    f32_encode(&mA64, a, n, n * ns, 64);
+    f32_encode(&mU128, ut, n * ns, NB, 128);
+    f32_encode(&mU64, ut, n * ns, NB, 64);
+    static DeviceOnce tcfg;
+    if (tcfg.needed())
+    {
+      MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::gemm_tma_kernel<128>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)f32u::gemm_tma_smem<128>()));
+      MPIRG_CUDA_CHECK(cudaFuncSetAttribute(f32u::gemm_tma_kernel<64>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)f32u::gemm_tma_smem<64>()));
+      tcfg.done();
+    }
+  }
   const int np = (n + NB - 1) / NB;
   BatchStride bs;
   bs.a = (size_t)n * n;
@@ -2049,7 +2071,28 @@ void launch_lu_batched_f32(float *a, int n, int ns, int *ipiv, int *perm, int2 *
     if (panel_rpt<float, NB>(n - k0) == 0)
       throw std::runtime_error("batched LU: n too large for a single-cluster panel");
     launch_panel<float, NB>(a, n, k0, jb, ipiv, mv, nm, info, s, ns, bs);
-    if (c0 < n)
+    if (c0 < n && tma)
+    {
+      const int t = n - c0;
+      prof_begin(KC_TRSM, s);
+      f32u::mt2_kernel<NB, false>
+          <<<dim3((t + f32u::MT_COLS - 1) / f32u::MT_COLS, 1, ns), 128, 0, s>>>(
+              a, n, k0, jb, c0, n, mv, nm, 0, ut, 0, a, bs, n * ns);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+      prof_end(KC_TRSM, s);
+      prof_begin(KC_GEMM, s);
+      if ((long)((t + 127) / 128) * ((t + 127) / 128) * ns >= 2 * 148)
+        f32u::gemm_tma_kernel<128>
+            <<<dim3((t + 127) / 128, (t + 127) / 128, ns), 256, f32u::gemm_tma_smem<128>(), s>>>(
+                mA128, mU128, a, n, k0, jb, 0, c0, n);
+      else
+        f32u::gemm_tma_kernel<64>
+            <<<dim3((t + 63) / 64, (t + 63) / 64, ns), 256, f32u::gemm_tma_smem<64>(), s>>>(
+                mA64, mU64, a, n, k0, jb, 0, c0, n);
+      MPIRG_CUDA_CHECK(cudaGetLastError());
+      prof_end(KC_GEMM, s);
+    }
+    else if (c0 < n)
     {
       prof_begin(KC_TRSM, s);
       lu_mt_kernel<float, NB><<<dim3((n - c0 + MT_COLS - 1) / MT_COLS, 1, ns), 128, 0, s>>>(

@@ -39,11 +39,20 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
                                                   const int2 *__restrict__ moves,
                                                   const int *__restrict__ nmoves, int kp,
                                                   float *__restrict__ ut, int ut_row,
-                                                  const float *__restrict__ Ls)
+                                                  const float *__restrict__ Ls,
+                                                  BatchStride bs = BatchStride{}, int ut_ld = 0)
 {
   constexpr int PER = (2 * NB + 31) / 32;
   constexpr int RL = (NB + 31) / 32;  // panel rows per lane
   __shared__ float L[NB][NB + 1];
+  // batched launches (config 5b): system blockIdx.z; its U12 copy occupies
+  // columns [z n, z n + n) of a ut with row pitch ut_ld = n * (systems)
+  A += (size_t)blockIdx.z * bs.a;
+  Ls += (size_t)blockIdx.z * bs.a;
+  moves += (size_t)blockIdx.z * bs.moves;
+  nmoves += (size_t)blockIdx.z * bs.nm;
+  ut += (size_t)blockIdx.z * n;
+  const size_t utp = ut_ld ? (size_t)ut_ld : (size_t)n;
   __shared__ float Lp[PEND ? NB : 1][NB + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int col0 = cb + blockIdx.x * MT_COLS + warp * 8;
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
   {
     const int kk = idx / MT_COLS, c = idx % MT_COLS;
     if (cbase + c < ce)
-      ut[(size_t)(ut_row + kk) * n + cbase + c] = L[kk][c];
+      ut[(size_t)(ut_row + kk) * utp + cbase + c] = L[kk][c];
   }
 }
 
@@ -245,6 +254,11 @@ __global__ void __launch_bounds__(256, BM == 128 ? 2 : 3)
   const int c0 = k0 + K;
   const int r0 = c0 + blockIdx.x * BM;
   const int cc0 = cb + blockIdx.y * BM;
+  // batched launches (config 5b): the systems are stored back to back, so the
+  // batch is one n x (n systems) matrix to the tensor maps; system blockIdx.z
+  // is a column offset of z n in both maps
+  const int zc = blockIdx.z * n;
+  A += (size_t)blockIdx.z * n * n;
   const int t = threadIdx.x;
   const int tx = t & 15, ty = t >> 4;
   const int nch = (K + GKC - 1) / GKC;
@@ -260,8 +274,8 @@ __global__ void __launch_bounds__(256, BM == 128 ? 2 : 3)
     for (int s = 0; s < GST && s < nch; ++s)
     {
       tc::mbar_expect_tx(&full[s], 2 * CHUNK);
-      tc::tma_load_2d(As + s * BM * GKC, &mapA, &full[s], r0, k0 + s * GKC);
-      tc::tma_load_2d(Bs + s * BM * GKC, &mapU, &full[s], cc0, ut_row + s * GKC);
+      tc::tma_load_2d(As + s * BM * GKC, &mapA, &full[s], r0, zc + k0 + s * GKC);
+      tc::tma_load_2d(Bs + s * BM * GKC, &mapU, &full[s], zc + cc0, ut_row + s * GKC);
     }
 
   float acc[TM][TM];
@@ -338,8 +352,8 @@ __global__ void __launch_bounds__(256, BM == 128 ? 2 : 3)
       {
         const int nx = ch + GST;
         tc::mbar_expect_tx(&full[st], 2 * CHUNK);
-        tc::tma_load_2d(As + st * BM * GKC, &mapA, &full[st], r0, k0 + nx * GKC);
-        tc::tma_load_2d(Bs + st * BM * GKC, &mapU, &full[st], cc0, ut_row + nx * GKC);
+        tc::tma_load_2d(As + st * BM * GKC, &mapA, &full[st], r0, zc + k0 + nx * GKC);
+        tc::tma_load_2d(Bs + st * BM * GKC, &mapU, &full[st], zc + cc0, ut_row + nx * GKC);
       }
     }
   }

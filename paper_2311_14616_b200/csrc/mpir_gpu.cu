@@ -201,6 +201,42 @@ struct mpirg_factorization
   int sg_seen = 0;
   cudaGraphExec_t sg_exec = nullptr;
 
+  // External storage (config 5b's batched LU factors many systems in shared
+  // group buffers; a worker handle then runs the refinement on one system's
+  // views of them). The handle's own matrices are kept and restored.
+  bool ext_bound = false;
+  void *own_a_high = nullptr, *own_a_low = nullptr;
+  int *own_ipiv = nullptr, *own_perm = nullptr;
+  void bind_external(const void *ah, void *al, int *ip, int *pm, double an1, int uf)
+  {
+    if (!ext_bound)
+    {
+      own_a_high = a_high;
+      own_a_low = a_low;
+      own_ipiv = ipiv;
+      own_perm = perm;
+      ext_bound = true;
+    }
+    a_high = const_cast<void *>(ah);
+    a_low = al;
+    ipiv = ip;
+    perm = pm;
+    anorm1 = an1;
+    underflow = uf;
+    residual_plan_make(rplan, cfg.tw, n, a_high);
+  }
+  void unbind()
+  {
+    if (!ext_bound)
+      return;
+    a_high = own_a_high;
+    a_low = own_a_low;
+    ipiv = own_ipiv;
+    perm = own_perm;
+    ext_bound = false;
+    residual_plan_make(rplan, cfg.tw, n, a_high);
+  }
+
   size_t tw_bytes() const { return elem_size(cfg.tw); }
   size_t tf_bytes() const { return elem_size(cfg.tf); }
   size_t tr_bytes() const { return elem_size(cfg.tr); }
@@ -256,6 +292,7 @@ struct mpirg_factorization
   void release()
   {
     cudaSetDevice(device);
+    unbind();
     for (void *p : {a_high, a_low, (void *)ipiv, (void *)perm, b, r, x, y, sol, comp, (void *)scal,
                     (void *)info})
       if (p)
@@ -1193,6 +1230,315 @@ static int batch_workers(int count, int n)
   return std::max(1, std::min(w, count));
 }
 
+// ---- config 5b, batched kernels ------------------------------------------------
+// <f64, f32, f64> scaled-correction batches (BASELINE 5b) take this path: the
+// systems are factored in groups of NS by batched launches (lu.cu
+// launch_lu_batched_f32: one launch per step for the whole group instead of
+// ~100 launches per system), double-buffered so that the refinement of group
+// g -- W host workers, each binding a reusable handle to one system's views of
+// the group buffers -- overlaps the LUs of groups g + 1 .. g + 3 on the device. Every
+// kernel is the single-system one: per-system results equal the sequential
+// ones bit for bit. MPIRG_BATCH_MODE=handles keeps the per-system path.
+static int batch_group_size(int count, int n)
+{
+  int g = n <= 1024 ? 128 : (n <= 2048 ? 32 : 8);
+  if (const char *e = std::getenv("MPIRG_BATCH_GROUP"))
+    g = std::max(1, std::atoi(e));
+  return std::max(1, std::min(g, count));
+}
+
+static bool batch_fast_ok(const mpirg_config &c, int n)
+{
+  if (const char *e = std::getenv("MPIRG_BATCH_MODE"))
+    if (std::string(e) == "handles")
+      return false;
+  const int otf = c.on_the_fly < 0 ? (c.tf == B16 || c.tf == c.tw) : c.on_the_fly;
+  return c.tw == B64 && c.tf == B32 && c.tr == B64 && otf == 0 && c.lu_mode == MPIRG_LU_EXACT &&
+         (c.nb == 0 || c.nb == 64) && n >= 64 && lu_batched_supported(B32, n);
+}
+
+struct BatchSlot
+{
+  float *a_low = nullptr, *ut = nullptr;
+  int *ipiv = nullptr, *perm = nullptr, *nmoves = nullptr;
+  int2 *moves = nullptr;
+  DevInfo *info = nullptr, *h_info = nullptr, *h_init = nullptr;
+  unsigned long long *norm = nullptr, *h_norm = nullptr;
+  cudaEvent_t done = nullptr;
+  void alloc(int ns, int n)
+  {
+    const int np = (n + 63) / 64;
+    a_low = dalloc<float>((size_t)ns * n * n);
+    ut = dalloc<float>((size_t)64 * ns * n);
+    ipiv = dalloc<int>((size_t)ns * n);
+    perm = dalloc<int>((size_t)ns * n);
+    nmoves = dalloc<int>((size_t)ns * np);
+    moves = dalloc<int2>((size_t)ns * np * 128);
+    info = dalloc<DevInfo>(ns);
+    norm = dalloc<unsigned long long>(ns);
+    MPIRG_CUDA_CHECK(cudaMallocHost(&h_info, sizeof(DevInfo) * ns));
+    MPIRG_CUDA_CHECK(cudaMallocHost(&h_init, sizeof(DevInfo) * ns));
+    MPIRG_CUDA_CHECK(cudaMallocHost(&h_norm, sizeof(unsigned long long) * ns));
+    for (int i = 0; i < ns; ++i)
+    {
+      h_init[i].overflow_index = ~0ull;
+      h_init[i].underflow = 0;
+      h_init[i].singular_col = INT_MAX;
+      h_init[i].nonfinite = 0;
+      h_init[i].pad = 0;
+    }
+    MPIRG_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  }
+  void release()
+  {
+    for (void *p : {(void *)a_low, (void *)ut, (void *)ipiv, (void *)perm, (void *)nmoves,
+                    (void *)moves, (void *)info, (void *)norm})
+      if (p)
+        cudaFree(p);
+    for (void *p : {(void *)h_info, (void *)h_init, (void *)h_norm})
+      if (p)
+        cudaFreeHost(p);
+    if (done)
+      cudaEventDestroy(done);
+  }
+};
+
+static int batch_ir_solve_fast(int count, int n, const mpirg_config &cfg_in, const char *a_dev,
+                               const char *b_dev, char *sol_dev, const BatchStage *stage,
+                               const mpirg_term_params *tp, double *rhist, double *dhist,
+                               int hist_capacity, int *rhist_len, int *reason, int *status,
+                               double *device_ms, mpirg_error *err, int dev)
+{
+  const int NS = batch_group_size(count, n), G = (count + NS - 1) / NS;
+  const int W = batch_workers(count, n);
+  const size_t nn = (size_t)n * n;
+  // NSLOT group buffers, each with its own stream: the LUs of consecutive
+  // groups overlap each other (one group's latency-bound panel launches run
+  // beside another's trailing updates) and the refinement of earlier groups
+  constexpr int NSLOT = 4;
+  BatchSlot slot[NSLOT];
+  cudaStream_t lstream[NSLOT] = {};
+  cudaEvent_t start = nullptr;
+  std::vector<mpirg_factorization *> handles(W, nullptr);
+  std::vector<cudaEvent_t> ends(W, nullptr);
+  std::mutex emu;
+  int first = MPIRG_OK;
+  mpirg_error first_err{};
+  auto note = [&](int st, const mpirg_error &e) {
+    std::lock_guard<std::mutex> lk(emu);
+    if (first == MPIRG_OK && st != MPIRG_OK)
+    {
+      first = st;
+      first_err = e;
+    }
+  };
+  auto cleanup = [&] {
+    for (auto *f : handles)
+      mpirg_factorization_destroy(f);
+    for (auto &e : ends)
+      if (e)
+        cudaEventDestroy(e);
+    for (int i = 0; i < NSLOT; ++i)
+    {
+      slot[i].release();
+      if (lstream[i])
+        cudaStreamDestroy(lstream[i]);
+    }
+    if (start)
+      cudaEventDestroy(start);
+  };
+  mpirg_config c = cfg_in;
+  c.device = dev;
+  {
+    mpirg_error e{};
+    const int st = guarded(&e, [&] {
+      MPIRG_CUDA_CHECK(cudaEventCreate(&start));
+      for (int i = 0; i < NSLOT && i < G; ++i)
+      {
+        MPIRG_CUDA_CHECK(cudaStreamCreateWithFlags(&lstream[i], cudaStreamNonBlocking));
+        slot[i].alloc(NS, n);
+      }
+      struct NoPartition  // the workers' handles share the whole GPU (lu.cu)
+      {
+        NoPartition() { lu_partition_allowed(false); }
+        ~NoPartition() { lu_partition_allowed(true); }
+      } no_partition;
+      for (int w = 0; w < W; ++w)
+      {
+        mpirg_error ce{};
+        const int cs = mpirg_factorization_create(&handles[w], n, &c, nullptr, 1, &ce);
+        if (cs != MPIRG_OK)
+          throw ApiError{cs, ce.message};
+        MPIRG_CUDA_CHECK(cudaEventCreate(&ends[w]));
+      }
+      MPIRG_CUDA_CHECK(cudaEventRecord(start, lstream[0]));
+      for (int i = 1; i < NSLOT && i < G; ++i)
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(lstream[i], start, 0));
+    });
+    if (st != MPIRG_OK)
+    {
+      cleanup();
+      if (err)
+        *err = e;
+      for (int i = 0; i < count; ++i)
+        status[i] = st;
+      return st;
+    }
+  }
+  // host-side pipeline state
+  std::atomic<int> next{0}, ready_upto{0}, failed{0};
+  std::vector<std::atomic<int>> finished(G);
+  for (auto &f : finished)
+    f.store(0);
+  auto group_size = [&](int g) { return std::min(NS, count - g * NS); };
+
+  auto enqueue = [&](int g) {
+    BatchSlot &S = slot[g % NSLOT];
+    cudaStream_t ls = lstream[g % NSLOT];
+    const int lo = g * NS, ns = group_size(g);
+    if (stage)
+      for (int ch = lo / stage->per; ch <= (lo + ns - 1) / stage->per; ++ch)
+        MPIRG_CUDA_CHECK(cudaStreamWaitEvent(ls, stage->ready[ch], 0));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(S.info, S.h_init, sizeof(DevInfo) * ns,
+                                     cudaMemcpyHostToDevice, ls));
+    MPIRG_CUDA_CHECK(cudaMemsetAsync(S.norm, 0, sizeof(unsigned long long) * ns, ls));
+    if (ns > 1)
+      launch_cast_norm(B64, B32, n, n, a_dev + (size_t)lo * nn * 8, S.a_low, S.norm, S.info, ls, 0,
+                       ns);
+    else
+      launch_cast_norm(B64, B32, n, n, a_dev + (size_t)lo * nn * 8, S.a_low, S.norm, S.info, ls);
+    launch_lu_batched_f32(S.a_low, n, ns, S.ipiv, S.perm, S.moves, S.nmoves, S.info, ls, S.ut);
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(S.h_info, S.info, sizeof(DevInfo) * ns,
+                                     cudaMemcpyDeviceToHost, ls));
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(S.h_norm, S.norm, sizeof(unsigned long long) * ns,
+                                     cudaMemcpyDeviceToHost, ls));
+    MPIRG_CUDA_CHECK(cudaEventRecord(S.done, ls));
+  };
+
+  auto worker = [&](int w) {
+    cudaSetDevice(dev);
+    mpirg_factorization *f = handles[w];
+    for (int idx; (idx = next.fetch_add(1)) < count;)
+    {
+      const int g = idx / NS, z = idx - g * NS;
+      while (ready_upto.load(std::memory_order_acquire) <= g && !failed.load())
+        std::this_thread::yield();
+      if (failed.load())
+      {
+        finished[g].fetch_add(1);
+        continue;
+      }
+      if (status[idx] == MPIRG_OK)
+      {
+        BatchSlot &S = slot[g % NSLOT];
+        mpirg_error e{};
+        mpirg_report rep{};
+        rep.sol = sol_dev + (size_t)idx * n * 8;
+        rep.sol_on_device = 1;
+        rep.rhist = rhist + (size_t)idx * hist_capacity;
+        rep.dhist = dhist + (size_t)idx * hist_capacity;
+        rep.hist_capacity = hist_capacity;
+        const int st = guarded(&e, [&] {
+          f->bind_external(a_dev + (size_t)idx * nn * 8, S.a_low + (size_t)z * nn,
+                           S.ipiv + (size_t)z * n, S.perm + (size_t)z * n,
+                           bits_to_d(S.h_norm[z]), S.h_info[z].underflow);
+          MPIRG_CUDA_CHECK(cudaMemcpyAsync(f->b, b_dev + (size_t)idx * n * 8, (size_t)n * 8,
+                                           cudaMemcpyDeviceToDevice, f->stream));
+          const mpirg_term_params t = tp ? *tp : mpirg_term_params{1.0, 1.0, 0.5, 10};
+          f->solve(t, &rep);
+        });
+        rhist_len[idx] = rep.rhist_len;
+        reason[idx] = rep.reason;
+        status[idx] = st;
+        note(st, e);
+      }
+      finished[g].fetch_add(1, std::memory_order_release);
+    }
+    cudaEventRecord(ends[w], f->stream);
+    cudaEventSynchronize(ends[w]);
+  };
+
+  for (int i = 0; i < count; ++i)
+  {
+    status[i] = MPIRG_OK;
+    rhist_len[i] = 0;
+    reason[i] = MPIRG_ITERATION_LIMIT;
+  }
+  std::vector<std::thread> pool;
+  for (int w = 0; w < W; ++w)
+    pool.emplace_back(worker, w);
+  {
+    mpirg_error e{};
+    const int st = guarded(&e, [&] {
+      int enq = 0;
+      for (int g = 0; g < G; ++g)
+      {
+        while (enq <= std::min(g + NSLOT - 1, G - 1))
+        {
+          if (enq >= NSLOT)  // the slot is free once every system of its last group is refined
+            while (finished[enq - NSLOT].load(std::memory_order_acquire) <
+                   group_size(enq - NSLOT))
+              std::this_thread::yield();
+          enqueue(enq);
+          ++enq;
+        }
+        BatchSlot &S = slot[g % NSLOT];
+        MPIRG_CUDA_CHECK(cudaEventSynchronize(S.done));
+        const int lo = g * NS, ns = group_size(g);
+        for (int z = 0; z < ns; ++z)
+        {
+          const DevInfo &hi = S.h_info[z];
+          mpirg_error se{};
+          if (hi.overflow_index != ~0ull)
+          {
+            double v = 0.0;
+            MPIRG_CUDA_CHECK(cudaMemcpy(&v, a_dev + ((size_t)(lo + z) * nn + hi.overflow_index) * 8,
+                                        8, cudaMemcpyDeviceToHost));
+            fill_err(&se, MPIRG_ERR_OVERFLOW,
+                     "value " + std::to_string(v) + " exceeds the largest finite b32 value", -1,
+                     v);
+            status[lo + z] = MPIRG_ERR_OVERFLOW;
+            note(MPIRG_ERR_OVERFLOW, se);
+          }
+          else if (hi.singular_col != INT_MAX)
+          {
+            fill_err(&se, MPIRG_ERR_SINGULAR, "pivot column is exactly zero", hi.singular_col);
+            status[lo + z] = MPIRG_ERR_SINGULAR;
+            note(MPIRG_ERR_SINGULAR, se);
+          }
+        }
+        ready_upto.store(g + 1, std::memory_order_release);
+      }
+    });
+    if (st != MPIRG_OK)
+    {
+      note(st, e);
+      failed.store(1);
+      for (int i = 0; i < count; ++i)
+        if (status[i] == MPIRG_OK && rhist_len[i] == 0)
+          status[i] = st;
+    }
+  }
+  for (auto &t : pool)
+    t.join();
+  double ms = 0.0;
+  for (int w = 0; w < W; ++w)
+  {
+    float m = 0.0f;
+    if (cudaEventElapsedTime(&m, start, ends[w]) == cudaSuccess)
+      ms = std::max(ms, (double)m);
+  }
+  cudaGetLastError();
+  if (device_ms)
+    *device_ms = ms;
+  cleanup();
+  if (err)
+    *err = first == MPIRG_OK ? mpirg_error{} : first_err;
+  if (first == MPIRG_OK)
+    fill_err(err, MPIRG_OK, "");
+  return first;
+}
+
 int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *a, const void *b,
                          int on_device, const mpirg_term_params *tp, void *sol, double *rhist,
                          double *dhist, int hist_capacity, int *rhist_len, int *reason,
@@ -1249,6 +1595,38 @@ int mpirg_batch_ir_solve(int count, int n, const mpirg_config *cfg, const void *
   if (!on_device)
     stage.make(count, n, tw, a, b);
   const bool staged = stage.ok;
+  if ((on_device || staged) && batch_fast_ok(*cfg, n))
+  {
+    cudaEventDestroy(start);
+    for (auto &ev : ends)
+      cudaEventDestroy(ev);
+    const int st = batch_ir_solve_fast(
+        count, n, *cfg, static_cast<const char *>(staged ? stage.a : a),
+        static_cast<const char *>(staged ? stage.b : b),
+        static_cast<char *>(staged ? stage.sol : sol), staged ? &stage : nullptr, tp, rhist, dhist,
+        hist_capacity, rhist_len, reason, status, device_ms, err, dev);
+    if (staged)
+    {
+      // runs of solved systems only: a failed system's slice of `sol` stays untouched
+      for (int lo = 0; lo < count;)
+      {
+        if (status[lo] != MPIRG_OK)
+        {
+          ++lo;
+          continue;
+        }
+        int hi = lo;
+        while (hi < count && status[hi] == MPIRG_OK)
+          ++hi;
+        const size_t off = (size_t)lo * n * tw;
+        cudaMemcpy(static_cast<char *>(sol) + off, static_cast<char *>(stage.sol) + off,
+                   (size_t)(hi - lo) * n * tw, cudaMemcpyDeviceToHost);
+        lo = hi;
+      }
+      stage.release();
+    }
+    return st;
+  }
   const void *a_src = staged ? stage.a : a;
   const void *b_src = staged ? stage.b : b;
   void *sol_dst = staged ? stage.sol : sol;

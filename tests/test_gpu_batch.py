@@ -122,3 +122,31 @@ def test_batch_from_host_buffers_equals_device_path(gpulib, pinned):
         assert np.array_equal(w, g)
     ok = np.repeat(want[3] == 0, n)
     assert np.array_equal(sol_h.numpy()[ok].view(np.uint64), sol_d.cpu().numpy()[ok].view(np.uint64))
+
+
+@pytest.mark.parametrize("group", ["5", "64"])
+def test_batched_kernels_equal_per_system_handles(gpulib, group, monkeypatch):
+    """The batched-kernel path (groups of systems factored by one launch per LU
+    step, refinement on reusable handles bound to the group buffers) against the
+    per-system-handle path: identical histories, reasons and solution bits,
+    through ragged groups and the double-buffered slots (group 5 of 23)."""
+    from paper_2311_14616_b200 import mpir
+    n, count = 320, 23
+    a = _systems(n, count, first=100)
+    a[11] = 0.0  # a singular system in the middle of a group
+    b = np.ones((count, n))
+    kw = dict(factor="single", resid_term=False, ce=10.0, litmax=10, raise_on_error=False)
+    monkeypatch.setenv("MPIRG_BATCH_MODE", "handles")
+    want = mpir.batch_solve(a, b, **kw)
+    monkeypatch.delenv("MPIRG_BATCH_MODE")
+    monkeypatch.setenv("MPIRG_BATCH_GROUP", group)
+    got = mpir.batch_solve(a, b, **kw)
+    assert [r["status"] for r in got] == [r["status"] for r in want]
+    assert want[11]["status"] != 0 and want[0]["status"] == 0
+    for w, g in zip(want, got):
+        if w["status"] != 0:
+            continue
+        assert g["reason"] == w["reason"]
+        assert [v.hex() for v in g["rhist"]] == [v.hex() for v in w["rhist"]]
+        assert [v.hex() for v in g["dhist"]] == [v.hex() for v in w["dhist"]]
+        assert np.array_equal(g["x"].view(np.uint64), w["x"].view(np.uint64))

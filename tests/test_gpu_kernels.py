@@ -263,3 +263,21 @@ def test_fast_division_matches_div_rn(prec, gpulib):
         rc = gpulib.mpirg_check_fast_div(prec, seed, 1 << 26, C.byref(bad), ex)
         assert rc == 0
         assert bad.value == 0, (prec, seed, bad.value, ex[0], ex[1])
+
+
+@pytest.mark.parametrize("n,alpha,col0,ncols", [(257, 800.0, 0, 257), (1000, 1.0, 0, 1000),
+                                                (1024, 1.0, 512, 300), (3, 2.5, 0, 3)])
+def test_device_greens_generator_bitwise(gpulib, n, alpha, col0, ncols):
+    """mpirg_gen_greens_operator_device against the host generator (itself
+    pinned to the reference's build_operator, tests/test_abi.py): every bit of
+    every entry, a column window included."""
+    import torch
+    from helpers import greens
+    want = greens(n, alpha)  # (n, n) Fortran order
+    out = torch.zeros(ncols * n, dtype=torch.float64, device="cuda")
+    st = gpulib.mpirg_gen_greens_operator_device(n, alpha, col0, ncols, out.data_ptr(), n, None)
+    torch.cuda.synchronize()
+    assert st == 0
+    got = out.cpu().numpy().reshape(ncols, n).T
+    assert np.array_equal(got.view(np.uint64), np.ascontiguousarray(
+        want[:, col0:col0 + ncols]).view(np.uint64))
