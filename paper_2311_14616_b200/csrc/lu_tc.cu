@@ -194,6 +194,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         continue;  // the other warpgroup's tile
       const int m = MT == 2 ? g : 0;
       const int rt = r0 + (t % mtiles) * Cfg::TM, ct = cb + (t / mtiles) * TN;
+      {
+        // while the tile's MMAs run, pull its C values towards L2: this warp's
+        // 32 rows of a column are 64 contiguous bytes (rows are 32-aligned)
+        const int prow = rt + m * 128 + q * 32;
+        if (prow < r1)
+          for (int c = lane; c < TN; c += 32)
+            if (ct + c < ce)
+            {
+              const h16 *pc = Cmat + (size_t)(ct + c) * n + prow;
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(pc));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + 16));
+            }
+      }
       tc::mbar_wait(&tfull[u], (j / NU) & 1);
       tc::fence_after();
       const int row = rt + m * 128 + q * 32 + lane;
