@@ -650,7 +650,8 @@ def respawn_under_torchrun(args):
         port = sk.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
-           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+           str(port), "--", os.path.abspath(__file__)] + sys.argv[1:]  # "--": bench's own
+    # flags (--n ...) must not be read as abbreviations of torchrun's
     sys.exit(subprocess.call(cmd))
 
 

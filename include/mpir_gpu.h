@@ -346,6 +346,9 @@ int mpirg_ffma_peak(double *tflops, double *ms);
 /* The same for binary64 DFMA (the roofline denominator of the fp64 chains:
  * residual and one-norm at small n, where rows/columns < lanes x SMSPs). */
 int mpirg_dfma_peak(double *tflops, double *ms);
+/* Dependent-chain latency of one FMA in cycles (MPIRG_B64 / MPIRG_B32): the
+ * per-column floor of the residual's and the substitutions' row chains. */
+int mpirg_fma_latency(int prec, double *cycles);
 /* Diagnostics: the binary32 trailing update (lu_f32.cuh gemm_tma_kernel) of
  * rows/columns [K, n) by K <= 128 steps on a zeroed n x n matrix, tile edge
  * `tile` (128, 64, or 0 = the LU's own choice), averaged over `reps` launches;

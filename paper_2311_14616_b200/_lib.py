@@ -177,6 +177,7 @@ PROTOTYPES = {
     "mpirg_ubench_gemm_f32": (_I, [_I, _I, _I, _I, C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "mpirg_dfma_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "mpirg_fma_latency": (_I, [_I, C.POINTER(C.c_double)]),
     "mpirg_check_fast_div": (_I, [C.c_int, C.c_ulonglong, C.c_longlong,
                                   C.POINTER(C.c_longlong), C.POINTER(C.c_double)]),
     "mpirg_gen_uniform_matrix": (None, [_I, _I, C.c_uint64, _D, _D, _P]),

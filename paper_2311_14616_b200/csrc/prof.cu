@@ -220,6 +220,53 @@ extern "C" int mpirg_dfma_peak(double *tflops, double *ms_out)
   return fma_peak<double>(tflops, ms_out, 1024);
 }
 
+// Dependent-chain latency of one FMA (cycles): the floor per column of the
+// residual's and the substitutions' row chains, which the reference's order
+// makes sequential.
+namespace
+{
+template <typename T>
+__global__ void fma_latency_kernel(T a, T b, T *out, long long *cycles)
+{
+  T s = a;
+  const long long t0 = clock64();
+#pragma unroll 64
+  for (int i = 0; i < 4096; ++i)
+  {
+    if constexpr (sizeof(T) == 8)
+      s = __fma_rn(s, b, a);
+    else
+      s = __fmaf_rn(s, b, a);
+  }
+  const long long t1 = clock64();
+  *out = s;
+  *cycles = t1 - t0;
+}
+}  // namespace
+
+extern "C" int mpirg_fma_latency(int prec, double *cycles)
+{
+  long long *dc = nullptr;
+  void *out = nullptr;
+  if (cudaMalloc(&dc, 8) != cudaSuccess || cudaMalloc(&out, 8) != cudaSuccess)
+    return MPIRG_ERR_CUDA;
+  for (int rep = 0; rep < 2; ++rep)
+  {
+    if (prec == MPIRG_B64)
+      fma_latency_kernel<double><<<1, 1>>>(1.0, 0.999, static_cast<double *>(out), dc);
+    else
+      fma_latency_kernel<float><<<1, 1>>>(1.0f, 0.999f, static_cast<float *>(out), dc);
+  }
+  long long h = 0;
+  const bool ok = cudaMemcpy(&h, dc, 8, cudaMemcpyDeviceToHost) == cudaSuccess;
+  cudaFree(dc);
+  cudaFree(out);
+  if (!ok)
+    return MPIRG_ERR_CUDA;
+  *cycles = (double)h / 4096.0;
+  return MPIRG_OK;
+}
+
 // ---- self-check of div_rcp (common.cuh) against the IEEE division ------------
 namespace
 {

@@ -63,3 +63,23 @@ def test_reference_arm_prints_one_json_line():
     assert line["impl"] == "reference" and line["unit"] == "s" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] in (
         "reference", "port")
+
+
+def test_bench_spawns_its_own_ranks_for_gpus_gt_1():
+    """`python bench.py --gpus 2` outside torchrun re-executes itself under
+    torch.distributed.run with two ranks on 127.0.0.1 (here the reference arm on
+    gloo: rank 0 prints the line, rank 1 exits without work)."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0", "--config", "cfg1",
+                          "--n", "192"], capture_output=True, text=True, timeout=300,
+                         env={k: v for k, v in os.environ.items()
+                              if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"]["n"] == 192 and line["value"] > 0
