@@ -507,7 +507,16 @@ def run_ours(args, world, rank, local):
             tfl = 2.0 * (n - K) ** 2 * K / (min(tms) * 1e-3) / 1e12
             tc_alone.append({"M": n - K, "N": n - K, "K": K, "ms": min(tms), "tflops": tfl,
                              "peak_tflops": gemm_peak,
-                             "frac": tfl / gemm_peak if gemm_peak else None})
+                             "frac": tfl / gemm_peak if gemm_peak else None,
+                             "algorithmic_bytes": 2 * (2 * (n - K) * K) + 4 * (n - K) ** 2})
+        try:  # DRAM traffic of the K = n/2 launch from the committed ncu --set full capture
+            trf = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            t4 = trf.get(args.config + "_tc", {}).get("tc_update_K%d" % (n // 2))
+            if t4 and tc_alone:
+                tc_alone[0]["traffic"] = t4["bytes_per_launch"]
+                tc_alone[0]["traffic_source"] = t4["capture"]
+        except Exception:
+            pass
         del scratch
 
     checks = None
