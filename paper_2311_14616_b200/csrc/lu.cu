@@ -753,37 +753,59 @@ void launch_panel(TG *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, De
   prof_end(KC_PANEL, s);
 }
 
-// Leaf of a tall panel: 8 columns, 512 threads per CTA, up to 16 CTAs.
-constexpr int LEAF = 8;
+// Leaf of a tall panel: LEAF columns, 512 threads per CTA, up to 16 CTAs. The
+// widest leaf whose rows fit the cluster's shared memory is used: 32 columns up
+// to 16384 rows (binary32), 16 up to 32768, 8 beyond -- a 64-column panel of
+// config 4 (n = 16384) is 2 leaves instead of 8.
 constexpr int LEAF_NT = 512;
-template <typename T>
+template <typename T, int LEAF>
 constexpr int leaf_max_rpt()
 {
-  return panel2::panel_dyn_smem<T, LEAF, 8, LEAF_NT>() <= 180 * 1024 ? 8 : 4;
+  int r = 8;
+  while (r > 1 && (sizeof(T) * (size_t)LEAF * r * LEAF_NT + 4096) > 180 * 1024)
+    r /= 2;
+  return r;
 }
 
-template <typename T>
+template <typename T, int LEAF>
+int leaf_capacity()
+{
+  return leaf_max_rpt<T, LEAF>() * LEAF_NT * panel_max_cs();
+}
+
+template <typename T, int LEAF>
 void launch_leaf(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, DevInfo *info,
                  cudaStream_t s)
 {
   const int m = n - k0;
-  int rpt = 1;
-  while (rpt * LEAF_NT * panel_max_cs() < m)
-    rpt *= 2;
-  if (rpt > leaf_max_rpt<T>())
-    throw std::runtime_error("LU panel: n too large for a single-cluster tall panel");
-  const int cs = std::max(1, (m + rpt * LEAF_NT - 1) / (rpt * LEAF_NT));
   prof_begin(KC_PANEL, s);
-  if (rpt == 1)
-    launch_panel_rpt<T, LEAF, 1, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
-  else if (rpt == 2)
-    launch_panel_rpt<T, LEAF, 2, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
-  else if (rpt == 4)
-    launch_panel_rpt<T, LEAF, 4, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+  if constexpr (LEAF == 8)
+  {
+    int rpt = 1;
+    while (rpt * LEAF_NT * panel_max_cs() < m)
+      rpt *= 2;
+    if (rpt > leaf_max_rpt<T, LEAF>())
+      throw std::runtime_error("LU panel: n too large for a single-cluster tall panel");
+    const int cs = std::max(1, (m + rpt * LEAF_NT - 1) / (rpt * LEAF_NT));
+    if (rpt == 1)
+      launch_panel_rpt<T, LEAF, 1, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+    else if (rpt == 2)
+      launch_panel_rpt<T, LEAF, 2, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+    else if (rpt == 4)
+      launch_panel_rpt<T, LEAF, 4, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+    else
+    {
+      if constexpr (leaf_max_rpt<T, LEAF>() >= 8)
+        launch_panel_rpt<T, LEAF, 8, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+    }
+  }
   else
   {
-    if constexpr (leaf_max_rpt<T>() >= 8)
-      launch_panel_rpt<T, LEAF, 8, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
+    // wider leaves only exist at their largest rows-per-thread (they are
+    // chosen when the panel is too tall for anything wider)
+    constexpr int rpt = leaf_max_rpt<T, LEAF>();
+    const int cs = std::max(1, (m + rpt * LEAF_NT - 1) / (rpt * LEAF_NT));
+    launch_panel_rpt<T, LEAF, rpt, LEAF_NT>(cs, a, n, k0, jb, ipiv, mv, nm, info, s);
   }
   prof_end(KC_PANEL, s);
 }
@@ -878,9 +900,9 @@ void launch_moves(T *a, int n, int cb, int ce, ColMap map, const int2 *mv, const
 // leaves of 8 columns (the same blocked right-looking order inside the
 // panel: leaf, its moves on the panel's left columns, mt + gemm on the
 // panel's right columns), composing the leaves' row moves in pp.
-template <typename T, int NB>
-void panel_tall(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, LuWorkspace &ws,
-                DevInfo *info, cudaStream_t s)
+template <typename T, int NB, int LEAF>
+void panel_tall_t(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, LuWorkspace &ws,
+                  DevInfo *info, cudaStream_t s)
 {
   const ColMap id{};
   const int m = n - k0;
@@ -894,13 +916,43 @@ void panel_tall(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, LuWor
     const int ks = k0 + l * LEAF, w = std::min(LEAF, jb - l * LEAF);
     int2 *smv = ws.smv + (size_t)l * 2 * LEAF;
     int *snm = ws.snm + l;
-    launch_leaf<T>(a, n, ks, w, ipiv, smv, snm, info, s);
+    launch_leaf<T, LEAF>(a, n, ks, w, ipiv, smv, snm, info, s);
     launch_moves<T, LEAF>(a, n, k0, ks, id, smv, snm, ws.pp, s);
     launch_mt<T, LEAF>(a, n, ks, w, ks + w, k0 + jb, id, smv, snm, s);
     launch_gemm<T, LEAF>(a, n, ks, w, ks + w, k0 + jb, id, s);
   }
   compact_moves_kernel<<<g, 256, 0, s>>>(ws.pp, k0, n, mv, nm);
   MPIRG_CUDA_CHECK(cudaGetLastError());
+}
+
+// MPIRG_TALL_LEAF=8 keeps the 8-column leaves at every height (A/B runs).
+static int tall_leaf_max()
+{
+  static const int v = [] {
+    const char *e = std::getenv("MPIRG_TALL_LEAF");
+    return e ? std::atoi(e) : 32;
+  }();
+  return v;
+}
+
+template <typename T, int NB>
+void panel_tall(T *a, int n, int k0, int jb, int *ipiv, int2 *mv, int *nm, LuWorkspace &ws,
+                DevInfo *info, cudaStream_t s)
+{
+  const int m = n - k0;
+  if constexpr (NB >= 32)
+    if (tall_leaf_max() >= 32 && m <= leaf_capacity<T, 32>())
+    {
+      panel_tall_t<T, NB, 32>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
+      return;
+    }
+  if constexpr (NB >= 16)
+    if (tall_leaf_max() >= 16 && m <= leaf_capacity<T, 16>())
+    {
+      panel_tall_t<T, NB, 16>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
+      return;
+    }
+  panel_tall_t<T, NB, 8>(a, n, k0, jb, ipiv, mv, nm, ws, info, s);
 }
 
 template <typename T, int NB>
@@ -2113,8 +2165,10 @@ void launch_lu_batched_f32(float *a, int n, int ns, int *ipiv, int *perm, int2 *
       prof_end(KC_GEMM, s);
     }
     prof_begin(KC_MOVES, s);
+    // few CTAs per system: most batches (diagonally dominant systems) have no
+    // row moves at all and every CTA only reads the count and leaves
     const int warps_needed = std::max(1, (k0 + 3) / 4);
-    const int grid = std::max(1, std::min((warps_needed + 7) / 8, 64));
+    const int grid = std::max(1, std::min((warps_needed + 7) / 8, 8));
     lu_apply_moves_kernel<float, NB><<<dim3(grid, 1, ns), 256, 0, s>>>(a, n, 0, k0, id, mv, nm,
                                                                      perm, bs);
     MPIRG_CUDA_CHECK(cudaGetLastError());
