@@ -185,6 +185,20 @@ void *mpirg_factorization_stream(const mpirg_factorization *f);
  * values of TW. tp == NULL uses the defaults. */
 int mpirg_ir_solve(mpirg_factorization *f, const void *b, int b_on_device,
                    const mpirg_term_params *tp, mpirg_report *rep, mpirg_error *err);
+/* Krylov corrections (krylov_ir.hpp:62-171, 297-318): MPFactorization's
+ * KrylovKind / basissize constructor arguments (mp_structures.hpp:108-151) as a
+ * call on an existing handle. With GMRES enabled, mpirg_ir_solve is
+ * krylov_ir_solve_report: each correction is one left-preconditioned GMRES
+ * solve (modified Gram-Schmidt, Givens rotations, at most `basissize` basis
+ * vectors, relative tolerance 1e-2) with the low-precision factors as the
+ * preconditioner, bitwise equal to the reference's. BiCGSTAB is not built
+ * (MPIRG_ERR_INVALID_CONFIG). khist (inner iteration counts, one per
+ * correction) and the breakdown flag of the last solve: _last_khist. */
+enum mpirg_krylov_kind { MPIRG_KRYLOV_NONE = 0, MPIRG_KRYLOV_GMRES = 1, MPIRG_KRYLOV_BICGSTAB = 2 };
+int mpirg_factorization_enable_krylov(mpirg_factorization *f, int kind, int basissize,
+                                      mpirg_error *err);
+int mpirg_factorization_last_khist(const mpirg_factorization *f, int *khist, int capacity,
+                                   int *len, int *breakdown);
 /* residual_tr(f, x, b) (ir_engine.hpp:277-287): r (n values of TR) = b - A x,
  * x and b in TW. Host or device buffers per on_device. */
 int mpirg_residual_tr(mpirg_factorization *f, const void *x, const void *b, void *r,

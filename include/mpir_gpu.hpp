@@ -296,7 +296,7 @@ public:
   }
   MPFactorization(const MPFactorization &) = delete;
   MPFactorization &operator=(const MPFactorization &) = delete;
-  MPFactorization(MPFactorization &&o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  MPFactorization(MPFactorization &&o) noexcept : h_(o.h_), krylov_(o.krylov_) { o.h_ = nullptr; }
   ~MPFactorization() { mpirg_factorization_destroy(h_); }
 
   // refactor (mp_structures.hpp:155-169): every device buffer is reused.
@@ -368,10 +368,20 @@ public:
     return static_cast<const TF *>(mpirg_factorization_packed_lu_device(h_));
   }
   const int *ipiv_device() const { return mpirg_factorization_ipiv_device(h_); }
+  // The Krylov workspace of mp_structures.hpp:134-151 (the reference passes
+  // KrylovKind / basissize to the constructor; mp_glu below does the same).
+  void enable_krylov(KrylovKind kind, int basissize)
+  {
+    mpirg_error e{};
+    throw_status(mpirg_factorization_enable_krylov(h_, static_cast<int>(kind), basissize, &e), e);
+    krylov_ = kind;
+  }
+  KrylovKind krylov_kind() const { return krylov_; }
   mpirg_factorization *handle() { return h_; }
 
 private:
   mpirg_factorization *h_ = nullptr;
+  KrylovKind krylov_ = KrylovKind::None;
 };
 
 template <typename TW, typename TF, typename TR = TW>
@@ -420,6 +430,33 @@ std::vector<TW> ir_solve(MPFactorization<TW, TF, TR> &f, const std::vector<TW> &
                          const TermParams &tp = {})
 {
   return ir_solve_report(f, b, tp).sol;
+}
+
+// mp_glu (mp_structures.hpp:221-225) and krylov_ir_solve_report
+// (krylov_ir.hpp:297-318): GMRES corrections preconditioned by the factors.
+template <typename TW, typename TF, typename TR = TW>
+MPFactorization<TW, TF, TR> mp_glu(const Matrix<TW> &a, int basissize = 10,
+                                   FactorOptions opts = {})
+{
+  MPFactorization<TW, TF, TR> f(a, opts);
+  f.enable_krylov(KrylovKind::Gmres, basissize);
+  return f;
+}
+
+template <typename TW, typename TF, typename TR>
+SolveReport<TW> krylov_ir_solve_report(MPFactorization<TW, TF, TR> &f, const std::vector<TW> &b,
+                                       const TermParams &tp = {})
+{
+  if (f.krylov_kind() == KrylovKind::None)
+    throw InvalidConfig("factorization was built without a Krylov workspace");
+  SolveReport<TW> rep = ir_solve_report(f, b, tp);
+  std::vector<int> kh(tp.litmax + 1);
+  int len = 0, brk = 0;
+  mpirg_factorization_last_khist(f.handle(), kh.data(), static_cast<int>(kh.size()), &len, &brk);
+  kh.resize(len < static_cast<int>(kh.size()) ? len : kh.size());
+  rep.khist = kh;
+  rep.breakdown = brk != 0;
+  return rep;
 }
 
 // residual_tr (ir_engine.hpp:277-287)
@@ -474,9 +511,10 @@ public:
                    KrylovKind kind = KrylovKind::None, int basissize = 10, int device = -1)
     : cfg_((cfg.validate(), cfg))  // validated before any allocation (runtime.cpp:69)
   {
-    (void)basissize;
-    if (kind != KrylovKind::None)
-      throw InvalidParameter("Krylov corrections are not part of the B200 IR hot path");
+    if (kind == KrylovKind::Bicgstab)
+      throw InvalidConfig("only GMRES corrections are built on the B200 path");
+    if (kind != KrylovKind::None && basissize < 1)
+      throw InvalidParameter("Krylov basis budget must be at least 1");
     if (cfg.tw == Precision::B16)
       throw InvalidConfig("working precision must be b64 or b32");
     if (a.rows() != a.cols())
@@ -498,10 +536,24 @@ public:
       const auto a32 = detail::to_b32(a.data(), a.size());
       throw_status(mpirg_factorization_create(&h_, a.rows(), &c, a32.data(), 0, &e), e);
     }
+    if (kind != KrylovKind::None)
+    {
+      const int st = mpirg_factorization_enable_krylov(h_, static_cast<int>(kind), basissize, &e);
+      if (st != MPIRG_OK)
+      {
+        mpirg_factorization_destroy(h_);
+        h_ = nullptr;
+        throw_status(st, e);
+      }
+      krylov_ = true;
+    }
   }
   AnyFactorization(const AnyFactorization &) = delete;
   AnyFactorization &operator=(const AnyFactorization &) = delete;
-  AnyFactorization(AnyFactorization &&o) noexcept : cfg_(o.cfg_), h_(o.h_) { o.h_ = nullptr; }
+  AnyFactorization(AnyFactorization &&o) noexcept : cfg_(o.cfg_), h_(o.h_), krylov_(o.krylov_)
+  {
+    o.h_ = nullptr;
+  }
   ~AnyFactorization() { mpirg_factorization_destroy(h_); }
 
   int n() const { return mpirg_factorization_n(h_); }
@@ -545,6 +597,15 @@ public:
         out.sol[i] = s32[i];
     out.reason = static_cast<StopReason>(r.reason);
     out.seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (krylov_)
+    {
+      out.khist.resize(cap > 0 ? cap : 1);
+      int len = 0, brk = 0;
+      mpirg_factorization_last_khist(h_, out.khist.data(), static_cast<int>(out.khist.size()),
+                                     &len, &brk);
+      out.khist.resize(len < static_cast<int>(out.khist.size()) ? len : out.khist.size());
+      out.breakdown = brk != 0;
+    }
     return out;
   }
 
@@ -574,6 +635,7 @@ public:
 private:
   PrecisionConfig cfg_;
   mpirg_factorization *h_ = nullptr;
+  bool krylov_ = false;
 };
 
 }  // namespace mpir::gpu

@@ -81,6 +81,9 @@ class CpuImpl:
         else:
             f("ir", _I, [_I, _I, _I, _I, _I, _I, _P, _P, _D, _D, _D, _I, _P, _DP, _DP, _IP,
                          _IP, _IP, _P, _DP, _IP, _IP, _DP, _DP, _DP])
+            if hasattr(self.lib, "ref_krylov_ir"):
+                f("krylov_ir", _I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _D, _D, _D, _I, _P, _DP,
+                                    _DP, _IP, _IP, _IP, _IP])
             f("build_operator", None, [_I, _D, _DP])
             f("integral_rhs", None, [_I, _D, _DP])
             f("matvec_compensated_f64", None, [_I, _DP, _DP, _DP])
@@ -196,6 +199,30 @@ class CpuImpl:
             "singular_col": sc.value, "bad_value": bad.value,
             "t_factor": tfac.value, "t_solve": tsol.value,
         }
+
+
+    def krylov_ir(self, tw, tf, tr, a, b, kind="gmres", basissize=10, resid_term=True, cr=1.0,
+                  ce=1.0, rmax=0.5, litmax=10):
+        """MPFactorization(a, opts, kind, basissize) + krylov_ir_solve_report
+        (compiled reference only)."""
+        n = b.size
+        a = fmat(a, DTYPES[tw])
+        b = np.ascontiguousarray(b, dtype=DTYPES[tw])
+        sol = np.zeros(n, dtype=DTYPES[tw])
+        cap = max(litmax, 1) + 1
+        rhist, dhist = np.zeros(cap), np.zeros(cap)
+        khist = np.zeros(cap, dtype=np.int32)
+        rlen, reason, brk = C.c_int(0), C.c_int(-1), C.c_int(0)
+        st = self._krylov_ir(tw, tf, tr, {"gmres": 1, "bicgstab": 2}[kind], basissize,
+                             int(resid_term), n, _ptr(a), _ptr(b), cr, ce, rmax, litmax,
+                             _ptr(sol), rhist.ctypes.data_as(_DP), dhist.ctypes.data_as(_DP),
+                             khist.ctypes.data_as(_IP), C.byref(rlen), C.byref(reason),
+                             C.byref(brk))
+        k = rlen.value
+        return {"status": STATUS.get(st, str(st)), "x": sol, "rhist": rhist[:k].copy(),
+                "dhist": dhist[:max(k - 1, 0)].copy(), "khist": khist[:max(k - 1, 0)].copy(),
+                "reason": REASONS[reason.value] if st == 0 else None,
+                "breakdown": bool(brk.value)}
 
 
 _cache: dict = {}

@@ -17,6 +17,7 @@
 #include "mpir/errors.hpp"
 #include "mpir/greens.hpp"
 #include "mpir/ir_engine.hpp"
+#include "mpir/krylov_ir.hpp"
 #include "mpir/matrix.hpp"
 #include "mpir/mp_structures.hpp"
 #include "mpir/precision.hpp"
@@ -197,6 +198,67 @@ int ir_typed(int on_the_fly, int resid_term, int n, const void *a, const void *b
   }
 }
 
+// MPFactorization(a, opts, kind, basissize) + krylov_ir_solve_report
+// (krylov_ir.hpp:297-318): the checker for the GPU GMRES-IR path.
+template <typename TW, typename TF, typename TR>
+int krylov_typed(int kind, int basissize, int resid_term, int n, const void *a, const void *b,
+                 double cr, double ce, double rmax, int litmax, void *sol, double *rhist,
+                 double *dhist, int *khist, int *rhist_len, int *reason, int *breakdown)
+{
+  *rhist_len = 0;
+  FactorOptions opts;
+  opts.resid_term = resid_term != 0;
+  TermParams tp;
+  tp.cr = cr;
+  tp.ce = ce;
+  tp.rmax = rmax;
+  tp.litmax = litmax;
+  try
+  {
+    tp.validate();
+  }
+  catch (const InvalidParameter &)
+  {
+    return ST_PARAM;
+  }
+  Matrix<TW> am = to_matrix<TW>(n, n, a);
+  const std::vector<TW> bv = to_vector<TW>(n, b);
+  try
+  {
+    MPFactorization<TW, TF, TR> f(std::move(am), opts,
+                                  kind == 2 ? KrylovKind::Bicgstab : KrylovKind::Gmres,
+                                  basissize);
+    const auto rep = krylov_ir_solve_report(f, bv, tp);
+    std::memcpy(sol, rep.sol.data(), sizeof(TW) * n);
+    for (size_t i = 0; i < rep.rhist.size(); ++i)
+      rhist[i] = rep.rhist[i];
+    for (size_t i = 0; i < rep.dhist.size(); ++i)
+      dhist[i] = rep.dhist[i];
+    for (size_t i = 0; i < rep.khist.size(); ++i)
+      khist[i] = rep.khist[i];
+    *rhist_len = static_cast<int>(rep.rhist.size());
+    *reason = static_cast<int>(rep.reason);
+    *breakdown = rep.breakdown ? 1 : 0;
+    return ST_OK;
+  }
+  catch (const NonFiniteResult &)
+  {
+    return ST_NONFINITE;
+  }
+  catch (const SingularPivot &)
+  {
+    return ST_SINGULAR;
+  }
+  catch (const OverflowDetected &)
+  {
+    return ST_OVERFLOW;
+  }
+  catch (const Error &)
+  {
+    return ST_OTHER;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -366,6 +428,32 @@ int ref_ir(int tw, int tf, int tr, int on_the_fly, int resid_term, int n, const 
   if (tw == 1 && tf == 2 && tr == 0)
     MPIR_REF_IR(float, Half, double);
 #undef MPIR_REF_IR
+  return ST_CONFIG;
+}
+
+int ref_krylov_ir(int tw, int tf, int tr, int kind, int basissize, int resid_term, int n,
+                  const void *a, const void *b, double cr, double ce, double rmax, int litmax,
+                  void *sol, double *rhist, double *dhist, int *khist, int *rhist_len,
+                  int *reason, int *breakdown)
+{
+#define MPIR_REF_KR(TW, TF, TR)                                                             \
+  return krylov_typed<TW, TF, TR>(kind, basissize, resid_term, n, a, b, cr, ce, rmax, litmax, \
+                                  sol, rhist, dhist, khist, rhist_len, reason, breakdown)
+  if (tw == 0 && tf == 0 && tr == 0)
+    MPIR_REF_KR(double, double, double);
+  if (tw == 0 && tf == 1 && tr == 0)
+    MPIR_REF_KR(double, float, double);
+  if (tw == 0 && tf == 2 && tr == 0)
+    MPIR_REF_KR(double, Half, double);
+  if (tw == 1 && tf == 1 && tr == 1)
+    MPIR_REF_KR(float, float, float);
+  if (tw == 1 && tf == 2 && tr == 1)
+    MPIR_REF_KR(float, Half, float);
+  if (tw == 1 && tf == 1 && tr == 0)
+    MPIR_REF_KR(float, float, double);
+  if (tw == 1 && tf == 2 && tr == 0)
+    MPIR_REF_KR(float, Half, double);
+#undef MPIR_REF_KR
   return ST_CONFIG;
 }
 

@@ -133,6 +133,9 @@ PROTOTYPES = {
     "mpirg_factorization_work_buf_device": (_P, [_H]),
     "mpirg_ir_solve": (_I, [_H, _P, _I, C.POINTER(mpirg_term_params), C.POINTER(mpirg_report), _E]),
     "mpirg_residual_tr": (_I, [_H, _P, _P, _P, _I, _E]),
+    "mpirg_factorization_enable_krylov": (_I, [_H, _I, _I, _E]),
+    "mpirg_factorization_last_khist": (_I, [_H, C.POINTER(C.c_int), _I, C.POINTER(C.c_int),
+                                            C.POINTER(C.c_int)]),
     "mpirg_demote": (_I, [_I, _I, _S, _P, _P, C.POINTER(C.c_int), _P, _E]),
     "mpirg_one_norm": (_I, [_I, _I, _I, _P, C.POINTER(C.c_double), _P, _E]),
     "mpirg_lu_factor": (_I, [_I, _I, _P, _P, _I, _I, _P, _E]),

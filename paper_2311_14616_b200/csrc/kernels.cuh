@@ -257,6 +257,31 @@ void residual_plan_free(ResidualPlan &p);
 void launch_residual(const ResidualPlan &p, int tr, const void *x, const void *b, void *r,
                      unsigned long long *rnorm_bits, cudaStream_t s);
 
+// ---- GMRES-IR corrections (krylov.cu; krylov_ir.hpp:62-171, 297-318) ---------
+struct GmresCtx
+{
+  int n = 0, tw = 0, tf = 0, bs = 0;
+  double rtol = 1e-2;       // gmres_correction_into's default
+  const void *a_high = nullptr;
+  const void *a_low = nullptr;
+  const int *perm = nullptr;
+  void *basis = nullptr;    // (bs + 1) x n values of TW
+  void *tmp = nullptr;      // n values of TW
+  void *dots = nullptr;     // bs + 2 device scalars of TW
+  void *h_dots = nullptr;   // pinned mirror
+  void *y = nullptr;        // substitution scratch
+  DevInfo *info = nullptr, *h_info = nullptr;
+  TrsvWorkspace *tws = nullptr;
+  cudaStream_t s = nullptr;
+  bool nonfinite = false;   // a preconditioner solve produced Inf/NaN
+};
+// w (n values of TW on the device): the residual on entry, the correction on
+// exit (d may alias r, krylov_ir.hpp:57). Synchronises the stream.
+void gmres_correction(GmresCtx &c, void *w, int *iters, bool *breakdown);
+void launch_demote_vec(int tw, int tr, int n, const void *r, void *w, cudaStream_t s);
+void launch_ir_update(int tw, int tr, int n, const void *w, void *x, unsigned long long *dnorm,
+                      unsigned long long *xnorm, cudaStream_t s);
+
 // ---- small vector kernels -------------------------------------------------
 // r = TR(b); x = 0; *bnorm_bits = ||r||_inf (refine_loop start, ir_engine.hpp:190-205)
 void launch_ir_init(int tw, int tr, int n, const void *b, void *r, void *x,

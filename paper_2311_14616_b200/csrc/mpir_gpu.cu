@@ -201,6 +201,35 @@ struct mpirg_factorization
   int sg_seen = 0;
   cudaGraphExec_t sg_exec = nullptr;
 
+  // GMRES-IR (krylov_ir.hpp): workspace carried by the factorization
+  // (mp_structures.hpp:134-151), enabled by mpirg_factorization_enable_krylov
+  int kry_kind = 0, kry_bs = 0;
+  void *kry_basis = nullptr, *kry_tmp = nullptr, *kry_w = nullptr, *kry_dots = nullptr;
+  void *kry_hdots = nullptr;  // pinned
+  std::vector<int> khist;
+  bool kry_breakdown = false;
+  void enable_krylov(int kind, int basissize)
+  {
+    free_krylov();
+    kry_kind = kind;
+    kry_bs = basissize;
+    kry_basis = dalloc_bytes((size_t)(basissize + 1) * n * tw_bytes());
+    kry_tmp = dalloc_bytes((size_t)n * tw_bytes());
+    kry_w = dalloc_bytes((size_t)n * tw_bytes());
+    kry_dots = dalloc_bytes((size_t)(basissize + 2) * 8);
+    MPIRG_CUDA_CHECK(cudaMallocHost(&kry_hdots, (size_t)(basissize + 2) * 8));
+  }
+  void free_krylov()
+  {
+    for (void *p : {kry_basis, kry_tmp, kry_w, kry_dots})
+      if (p)
+        cudaFree(p);
+    if (kry_hdots)
+      cudaFreeHost(kry_hdots);
+    kry_basis = kry_tmp = kry_w = kry_dots = kry_hdots = nullptr;
+    kry_kind = kry_bs = 0;
+  }
+
   // External storage (config 5b's batched LU factors many systems in shared
   // group buffers; a worker handle then runs the refinement on one system's
   // views of them). The handle's own matrices are kept and restored.
@@ -293,6 +322,7 @@ struct mpirg_factorization
   {
     cudaSetDevice(device);
     unbind();
+    free_krylov();
     for (void *p : {a_high, a_low, (void *)ipiv, (void *)perm, b, r, x, y, sol, comp, (void *)scal,
                     (void *)info})
       if (p)
@@ -526,6 +556,8 @@ struct mpirg_factorization
       rep->reason = reason;
     };
 
+    khist.clear();
+    kry_breakdown = false;
     MPIRG_CUDA_CHECK(cudaEventRecord(ev[2], s));
     MPIRG_CUDA_CHECK(cudaMemsetAsync(scal + 1, 0, sizeof(unsigned long long) * (ns - 1), s));
     reset_info(info, s);
@@ -562,7 +594,49 @@ struct mpirg_factorization
         a.lps = 1;
         a.rho_bits = it == 0 ? scal + 1 : scal + 2 + 3 * (it - 1) + 2;
       }
-      launch_trsv(a, tws, s);
+      if (kry_kind == 0)
+        launch_trsv(a, tws, s);
+      else
+      {
+        // krylov_ir_solve_report's corrector (krylov_ir.hpp:303-317): w = TW(r),
+        // d = GMRES(A, M; w), x += TR(d), ||d||_inf
+        launch_demote_vec(cfg.tw, cfg.tr, n, r, kry_w, s);
+        GmresCtx g;
+        g.n = n;
+        g.tw = cfg.tw;
+        g.tf = cfg.tf;
+        g.bs = kry_bs;
+        g.a_high = a_high;
+        g.a_low = a_low;
+        g.perm = perm;
+        g.basis = kry_basis;
+        g.tmp = kry_tmp;
+        g.dots = kry_dots;
+        g.h_dots = kry_hdots;
+        g.y = y;
+        g.info = info;
+        g.h_info = h_info;
+        g.tws = &tws;
+        g.s = s;
+        int its = 0;
+        bool brk = false;
+        gmres_correction(g, kry_w, &its, &brk);
+        if (g.nonfinite)
+        {
+          if (it == 0)
+          {
+            MPIRG_CUDA_CHECK(cudaMemcpy(h_scal + 1, scal + 1, sizeof(unsigned long long),
+                                        cudaMemcpyDeviceToHost));
+            rhist.push_back(bits_to_d(h_scal[1]));
+          }
+          emit(MPIRG_ITERATION_LIMIT);
+          throw ApiError{MPIRG_ERR_NONFINITE,
+                         "promoting substitution produced a non-finite entry"};
+        }
+        khist.push_back(its);
+        kry_breakdown = kry_breakdown || brk;
+        launch_ir_update(cfg.tw, cfg.tr, n, kry_w, x, slot + 0, slot + 1, s);
+      }
       launch_residual(rplan, cfg.tr, x, b, r, slot + 2, s);
       const int nread = 2 + 3 * (it + 1);
       MPIRG_CUDA_CHECK(cudaMemcpyAsync(h_scal + 1, scal + 1,
@@ -2117,4 +2191,40 @@ int mpirg_tc_gemm(int n, void *a, int r0, int r1, int cb, int ce, int k0, int K,
     tc_plan_make(plan, a, n);
     tc_gemm(plan, r0, r1, cb, ce, k0, K, static_cast<cudaStream_t>(stream));
   });
+}
+
+// GMRES-IR (krylov_ir.hpp; MPFactorization's KrylovKind / basissize arguments,
+// mp_structures.hpp:108-151): attaches the Krylov workspace to a handle; every
+// later mpirg_ir_solve takes its corrections from the preconditioned GMRES
+// instead of the plain substitution (krylov_ir_solve_report).
+int mpirg_factorization_enable_krylov(mpirg_factorization *f, int kind, int basissize,
+                                      mpirg_error *err)
+{
+  return guarded(err, [&] {
+    MPIRG_CUDA_CHECK(cudaSetDevice(f->device));
+    if (kind == MPIRG_KRYLOV_NONE)
+    {
+      f->free_krylov();
+      return;
+    }
+    if (basissize < 1)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "Krylov basis budget must be at least 1"};
+    if (kind != MPIRG_KRYLOV_GMRES)
+      throw ApiError{MPIRG_ERR_INVALID_CONFIG,
+                     "only GMRES corrections are built on the B200 path"};
+    f->enable_krylov(kind, basissize);
+  });
+}
+
+int mpirg_factorization_last_khist(const mpirg_factorization *f, int *khist, int capacity,
+                                   int *len, int *breakdown)
+{
+  const int k = (int)f->khist.size();
+  for (int i = 0; i < k && i < capacity; ++i)
+    khist[i] = f->khist[i];
+  if (len)
+    *len = k;
+  if (breakdown)
+    *breakdown = f->kry_breakdown ? 1 : 0;
+  return MPIRG_OK;
 }

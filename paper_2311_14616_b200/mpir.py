@@ -11,9 +11,11 @@ import. Everything numeric runs on the GPU through libmpir_gpu.so:
 * ``Factorization.solve`` -> ir_solve_report (ir_engine.hpp:291-297).
 * ``solve`` -> factor once and refine (bindings.cpp:221-240).
 
-Krylov corrections (``krylov=...``) and ``direct_solve`` are outside the
-B200 hot path this build covers; they raise
-InvalidParameter instead of silently running on the CPU.
+``krylov="gmres"`` attaches the reference's GMRES workspace: ``solve`` is then
+krylov_ir_solve_report (krylov_ir.hpp:297-318) with GMRES corrections on the
+device, bitwise equal to the reference, and the report carries ``khist``.
+BiCGSTAB corrections and ``direct_solve`` are not built (SURVEY.md section
+8(f)); they raise instead of silently running on the CPU.
 """
 from __future__ import annotations
 
@@ -122,8 +124,14 @@ class Factorization:
     def __init__(self, a, *, working="double", factor=None, residual=None, on_the_fly=None,
                  resid_term=True, krylov=None, basissize=10, lu_mode="exact", nb=0,
                  device=None):
-        if krylov is not None:
-            raise InvalidParameter("Krylov corrections are not part of the B200 IR hot path")
+        kind = {None: 0, "none": 0, "gmres": 1, "bicgstab": 2}.get(
+            krylov if krylov is None else str(krylov).lower(), -1)
+        if kind < 0:
+            raise InvalidParameter("unknown Krylov kind (gmres, bicgstab or none)")
+        if kind == 2:
+            raise InvalidConfig("only GMRES corrections are built on the B200 path")
+        if kind and int(basissize) < 1:
+            raise InvalidParameter("Krylov basis budget must be at least 1")
         cfg = resolve_config(parse_precision(working),
                              None if factor is None else parse_precision(factor),
                              None if residual is None else parse_precision(residual),
@@ -144,6 +152,10 @@ class Factorization:
                                                 dev.data_ptr(), 1, C.byref(err))
         L.check(st, err)
         L.lib().mpirg_factorization_config(self._h, C.byref(self._cfg))
+        self._krylov = kind
+        if kind:
+            L.check(L.lib().mpirg_factorization_enable_krylov(self._h, kind, int(basissize),
+                                                              C.byref(err)), err)
 
     @classmethod
     def _allocate(cls, n: int, cfg) -> "Factorization":
@@ -152,6 +164,7 @@ class Factorization:
         self = cls.__new__(cls)
         self._n = n
         self._cfg = cfg
+        self._krylov = 0
         self._h = C.c_void_p()
         err = L.mpirg_error()
         st = L.lib().mpirg_factorization_create(C.byref(self._h), n, C.byref(cfg), None, 1,
@@ -237,7 +250,14 @@ class Factorization:
         rhist = [rh[i] for i in range(rep.rhist_len)]
         dhist = [dh[i] for i in range(rep.dhist_len)]
         L.check(st, err, rhist=rhist, dhist=dhist)
-        return {"x": sol.double().cpu().numpy(), "rhist": rhist, "dhist": dhist, "khist": [],
+        khist, breakdown = [], False
+        if getattr(self, "_krylov", 0):
+            kh = (C.c_int * cap)()
+            klen, brk = C.c_int(0), C.c_int(0)
+            L.lib().mpirg_factorization_last_khist(self._h, kh, cap, C.byref(klen), C.byref(brk))
+            khist, breakdown = [kh[i] for i in range(min(klen.value, cap))], bool(brk.value)
+        return {"x": sol.double().cpu().numpy(), "rhist": rhist, "dhist": dhist, "khist": khist,
+                "breakdown": breakdown,
                 "reason": L.REASONS[rep.reason], "seconds": sec, "device_ms": rep.solve_ms}
 
     def refactor(self, a) -> None:
