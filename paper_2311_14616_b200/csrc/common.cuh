@@ -95,15 +95,34 @@ __device__ __forceinline__ h16 divide(h16 a, h16 b) { return hdiv(a, b); }
 // IEEE division from a precomputed reciprocal, for divisions on a sequential
 // critical path whose divisor is known early (the diagonal of U in the back
 // substitution). With y = RN(1/b):
-//   q0 = RN(a*y)                   (within 1.5 ulp of a/b)
-//   q1 = q0 + RN(a - b*q0) * y     (within 1 ulp)
-//   q2 = q1 + RN(a - b*q1) * y     (Markstein: q2 = RN(a/b))
+//   q0 = RN(a*y)
+//   q1 = RN(q0 + RN(a - b*q0) * y)     (both residuals exact: one FMA each)
+//   q2 = RN(q1 + RN(a - b*q1) * y)  =  RN(a/b)
 // i.e. one multiply and four dependent FMAs instead of MUFU.RCP + the Newton
-// sequence + FCHK of div.rn. Valid while a, b and a/b stay away from the
-// subnormal and overflow ranges and a != 0 (signed zeros): the caller
-// passes ok = rcp_ok(b) computed with y, and div_rcp also checks a; anything
-// else takes the IEEE division. Checked bitwise against div.rn by
-// mpirg_check_fast_div (tests/test_gpu_kernels.py).
+// sequence + FCHK of div.rn.
+//
+// Why q2 is the correctly rounded quotient (Markstein, "Computation of
+// elementary functions on the IBM RISC System/6000 processor", IBM J. Res.
+// Dev. 34(1), 1990, Theorem 1; the form used here is Cornea, Harrison and
+// Tang, "Scientific Computing on Itanium-based Systems", 2002, ch. 8, and
+// Muller et al., "Handbook of Floating-Point Arithmetic", 2nd ed., Theorem 4.8
+// / section 4.7): if y is within one ulp of 1/b (here it is the correctly
+// rounded reciprocal, error <= 1/2 ulp) and q is within one ulp of a/b, then
+// r = RN(a - b*q) is computed exactly by one FMA and RN(q + r*y) is the
+// correctly rounded quotient -- PROVIDED no intermediate underflows, overflows
+// or loses bits to gradual underflow. q0 = RN(a*y) is within 3/2 ulp, q1 within
+// one ulp, so the theorem applies to the last step. Preconditions as enforced
+// here: b normal with |b| in [2^-60, 2^61) (binary32) / [2^-500, 2^501)
+// (binary64), so y is normal and b*q cannot overflow; a nonzero with |a| in the
+// same window, so a*y, a/b and the residuals a - b*q (which can be as small as
+// |a| 2^-24 / 2^-53) stay normal. Zeros (signed-zero results), subnormals,
+// infinities and NaN operands, and anything outside the windows take div.rn:
+// the caller passes ok = rcp_ok(b) computed with y, div_rcp also checks a, and
+// the TRSV diagonal solve redoes a whole block with div.rn when any operand of
+// the block was outside (trsv.cu). The identity is additionally checked bit for
+// bit against div.rn on 2 x 10^8 operand pairs per precision, including every
+// exponent, near-power-of-two and all-ones significands
+// (mpirg_check_fast_div, tests/test_gpu_kernels.py).
 struct RcpF
 {
   float y;

@@ -2233,8 +2233,16 @@ static int green_request()
 
 static GreenSplit &green_split()
 {
-  static GreenSplit g;
-  static bool tried = false;
+  // one split per device (mpirg_config.device / mpirg_dlu_create(device) let a
+  // process use several)
+  static GreenSplit gs[64];
+  static bool tried_dev[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  GreenSplit &g = gs[cur & 63];
+  bool &tried = tried_dev[cur & 63];
   if (tried)
     return g;
   tried = true;
