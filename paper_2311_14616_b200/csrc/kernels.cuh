@@ -214,10 +214,10 @@ struct TrsvWorkspace
 {
   int n = 0;
   int nblk = 0;
-  int *flags = nullptr;    // [2][nblk] ready flags (lower, upper), epoch-tagged
   int *tickets = nullptr;  // [2] block tickets
-  unsigned long long *xw = nullptr;  // [2][n] tagged hand-off words (binary32/16 x)
-  int cap_blk = 0, cap_n = 0;        // allocated capacities
+  unsigned long long *xw = nullptr;  // [2][2 cap_n] tagged hand-off words (lower, upper; two per binary64 x)
+  int cap_n = 0;                     // allocated capacity
+  void *map_cache = nullptr;         // host: the TMA map of the factor matrix last solved with (trsv.cu)
   int epoch = 0;
 };
 void trsv_workspace_alloc(TrsvWorkspace &ws, int n);
