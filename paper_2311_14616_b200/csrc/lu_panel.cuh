@@ -30,6 +30,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "lu_spec.cuh"
 
 namespace mpirg
 {
@@ -38,7 +39,6 @@ namespace panel2
 
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
-constexpr int MAXCS = 16;
 constexpr int IB = 8;
 
 // Per-step message of one CTA: its candidate and the candidate's current
@@ -109,21 +109,6 @@ __device__ __forceinline__ unsigned long long cand_bits(double a)
   // +0.0 and positive values map above 0 so "no candidate" can be 0.
   return (unsigned long long)__double_as_longlong(a) + 1ull;
 }
-
-// Candidate key of |a| (a non-NaN): its IEEE bits + 1, so 0 means "none" and
-// the unsigned order is the numeric order of the (non-negative) magnitudes.
-__device__ __forceinline__ unsigned long long mag_key(float a)
-{
-  return (unsigned long long)__float_as_uint(fabsf(a)) + 1ull;
-}
-__device__ __forceinline__ unsigned long long mag_key(double a)
-{
-  return (unsigned long long)__double_as_longlong(fabs(a)) + 1ull;
-}
-__device__ __forceinline__ unsigned long long mag_key(h16 a) { return mag_key(h2f(a)); }
-__device__ __forceinline__ bool is_nan_t(float a) { return isnan(a); }
-__device__ __forceinline__ bool is_nan_t(double a) { return isnan(a); }
-__device__ __forceinline__ bool is_nan_t(h16 a) { return (a.bits & 0x7c00u) == 0x7c00u && (a.bits & 0x3ffu); }
 
 // Warp-uniform argmax over (key, pos): the largest key, ties to the lowest
 // position. redux.sync does each reduction in one instruction; 64-bit keys
@@ -218,7 +203,6 @@ __device__ __forceinline__ uint32_t cluster_size()
   return r;
 }
 
-__host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Dynamic shared memory: P[NB][R] (this CTA's rows, column-major) + Ub[IB][NB]
 // (the block's pivot rows: block columns from the step messages, right
@@ -226,7 +210,12 @@ __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(1
 template <typename T, int NB, int RPT, int NTX = NT>
 __host__ __device__ constexpr size_t panel_dyn_smem()
 {
-  return a16(sizeof(T) * (size_t)NB * RPT * NTX) + a16(sizeof(T) * (size_t)IB * NB);
+  const size_t exact = a16(sizeof(T) * (size_t)NB * RPT * NTX) + a16(sizeof(T) * (size_t)IB * NB);
+  // the whole-panel speculation (below) keeps its own layout in the same buffer
+  const size_t spec = (sizeof(T) == 4 && NB == 64 && RPT == 1 && NTX == 256)
+                          ? a16(2 * sizeof(float) * (size_t)NB * NB + 256) + sizeof(float) * (size_t)2 * NB * NTX
+                          : 0;
+  return exact > spec ? exact : spec;
 }
 
 #ifdef MPIRG_DEBUG_PANEL
@@ -268,6 +257,167 @@ __device__ __forceinline__ TG panel_out(T v)
     return v;
   else
     return demote<TG, T>(v);
+}
+
+// Returns true when the panel was completed here (A, ipiv, info updated).
+// Row mapping of this pass (its own, not the exchange algorithm's): warp 0 of
+// every CTA has the diagonal block only; the m - NB rows below it are dealt to
+// the other NTX - 32 threads of the CS CTAs, consecutive rows to consecutive
+// threads, in up to NR slots per thread.
+template <int NB, int NR, int NTX, typename TG>
+__device__ __forceinline__ bool whole_panel_spec(TG *__restrict__ A, int n, int k0, unsigned char *dsm,
+                                                 int *__restrict__ ipiv, DevInfo *info, int CS,
+                                                 int rank)
+{
+  constexpr int NBLK = NB / 8;
+  constexpr int RT = NTX - 32;  // row threads per CTA
+  auto &sh = *reinterpret_cast<SpecShared<NB> *>(dsm);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float *stash = reinterpret_cast<float *>(dsm + a16(sizeof(SpecShared<NB>))) + t;
+#ifdef MPIRG_DEBUG_PANEL
+  const long long w0 = clock64();
+  long long w1 = w0, w2 = w0, w3 = w0;
+#endif
+  if (t == 0)
+  {
+    sh.prog = 0;
+    sh.abort = 0;
+    sh.zj = NB;
+  }
+  __syncthreads();
+  bool beaten = false, stop = false;
+  // an equal share of the rows below the block per CTA (contiguous), slot q of
+  // thread t - 32 = the share's row q RT + t - 32: only the first warps of a
+  // CTA have second-slot rows
+  const int below = n - k0 - NB;
+  const int per = (below + CS - 1) / CS;
+  const int base = k0 + NB + rank * per;
+  int row[NR];
+  bool act[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q)
+  {
+    const int i = q * RT + (t - 32);
+    row[q] = base + i;
+    act[q] = warp != 0 && i < per && row[q] < n;
+  }
+  if (warp == 0)
+  {
+    float D[2][NBLK][8];
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+    {
+      D[0][c / 8][c % 8] = panel_in<float, TG>(A[(size_t)(k0 + c) * n + k0 + lane]);
+      D[1][c / 8][c % 8] = panel_in<float, TG>(A[(size_t)(k0 + c) * n + k0 + lane + 32]);
+    }
+    int zj = NB;
+#ifdef MPIRG_DEBUG_PANEL
+    w1 = clock64();
+#endif
+    spec_diag_phase<NB, 0>(D, sh, lane, rank == 0, beaten, zj, stop);
+    spec_diag_phase<NB, 1>(D, sh, lane, rank == 0, beaten, zj, stop);
+#ifdef MPIRG_DEBUG_PANEL
+    w2 = clock64();
+#endif
+    if (rank == 0 && lane == 0)
+      sh.zj = zj;
+    beaten = false;  // (recorded in sh.abort)
+  }
+  else if (__any_sync(0xffffffffu, act[0]))
+  {
+    const bool two = NR > 1 && __any_sync(0xffffffffu, act[NR - 1]);  // this warp has second-slot rows
+    // the rows go to the stash, eight columns of loads in flight at a time
+#pragma unroll 1
+    for (int c0 = 0; c0 < NB; c0 += 8)
+    {
+      float tmp[NR][8];
+#pragma unroll
+      for (int q = 0; q < NR; ++q)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          tmp[q][e] = act[q] ? panel_in<float, TG>(A[(size_t)(k0 + c0 + e) * n + row[q]]) : 0.0f;
+#pragma unroll
+      for (int q = 0; q < NR; ++q)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          stash[(size_t)(q * NB + c0 + e) * NTX] = tmp[q][e];
+    }
+#pragma unroll 1
+    for (int b = 0; b < NBLK; ++b)
+    {
+      if (b > 0 && __any_sync(0xffffffffu, beaten))
+        sh.abort = 1;
+      while (sh.prog < 8 * (b + 1) && !sh.abort)
+        __nanosleep(40);
+      if (sh.abort)
+        stop = true;
+      if (stop)
+        break;
+      __threadfence_block();
+      if (two)
+        spec_rows_block<NB, NR, NTX>(stash, act, sh.U, b, beaten);
+      else
+      {
+        const bool act1[1] = {act[0]};
+        spec_rows_block<NB, 1, NTX>(stash, act1, sh.U, b, beaten);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, beaten))
+    sh.abort = 1;
+#ifdef MPIRG_DEBUG_PANEL
+  w3 = clock64();
+#endif
+  __syncthreads();
+#ifdef MPIRG_DEBUG_PANEL
+  if (t == 0 && rank == 0)
+    printf("spec k0=%d rank=%d t=%d abort=%d load=%lld diag=%lld rows=%lld sync=%lld\n", k0, rank, t, sh.abort, w1 - w0,
+           w2 - w1, w3 - w2, clock64() - w3);
+#endif
+  // verdict
+  bool bad = sh.abort != 0;
+  if (CS > 1)
+  {
+    if (warp == 0 && lane < CS)
+    {
+      const uint32_t v = bad ? 1u : 0u;
+      asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(
+                       mapa(smem_addr(&sh.verdict[rank]), (uint32_t)lane)),
+                   "r"(v)
+                   : "memory");
+    }
+    cluster_sync_all();
+    bad = false;
+    for (int i = 0; i < CS; ++i)
+      bad |= sh.verdict[i] != 0u;
+  }
+  if (bad)
+  {
+    __syncthreads();  // every thread has read the verdicts before the panel is staged over them
+    return false;
+  }
+  // clean: write the panel back; ipiv = identity, no row moves
+#pragma unroll
+  for (int q = 0; q < NR; ++q)
+    if (act[q])
+    {
+#pragma unroll 8
+      for (int c = 0; c < NB; ++c)
+        A[(size_t)(k0 + c) * n + row[q]] = panel_out<TG, float>(stash[(size_t)(q * NB + c) * NTX]);
+    }
+  if (rank == 0)
+  {
+    for (int idx = t; idx < NB * NB; idx += NTX)
+    {
+      const int c = idx / NB, r = idx - c * NB;
+      A[(size_t)(k0 + c) * n + k0 + r] = panel_out<TG, float>(c >= r ? sh.U[r][c] : sh.Dg[r][c]);
+    }
+    if (t < NB)
+      ipiv[k0 + t] = k0 + t;
+    if (t == 0 && sh.zj < NB)
+      atomicMin(&info->singular_col, k0 + sh.zj);
+  }
+  return true;
 }
 
 template <typename T, int NB, int RPT, int NTX = NT, typename TG = T>
@@ -318,6 +468,27 @@ __global__ void __launch_bounds__(NTX, 1)
   {
     const int g = row0 + t + q * NT;
     pos[q] = g < n ? g : -1;  // -1: no row
+  }
+  // Whole-panel speculation first (see above); a clean panel ends here.
+  int spec_skip = 0;
+  if constexpr (whole_spec_eligible<T, NB, RPT, NTX>())
+  {
+    // DevInfo::pad: panels still to skip (low byte) | back-off level (next
+    // byte): a beaten panel makes the next `level` panels not try (level 1, 2,
+    // 4, 8 on consecutive failures), a clean one resets it. Every CTA reads it
+    // before anyone writes it (kernel end).
+    spec_skip = info->pad;
+    if (spec_ok && (spec_skip & 0xff) == 0 && jb == NB)
+    {
+      if (whole_panel_spec<NB, 2, NTX, TG>(A, n, k0, dsm, ipiv, info, CS, rank))
+      {
+        if (rank == 0 && t == 0 && spec_skip != 0)
+          info->pad = 0;
+        return;
+      }
+      const int level = min(max(2 * (spec_skip >> 8), 1), kSpecSkip);
+      spec_skip = -((level << 8) | level);  // beaten: negative = store at kernel end
+    }
   }
   // Stage the panel rows in shared memory (coalesced columns, 8 columns of
   // loads in flight per batch).
@@ -987,6 +1158,16 @@ __global__ void __launch_bounds__(NTX, 1)
   if (multi)
   {
     cluster_sync_all();  // no CTA may exit while peers can still write its inbox
+  }
+  if constexpr (whole_spec_eligible<T, NB, RPT, NTX>())
+  {
+    if (rank == 0 && t == 0)
+    {
+      if (spec_skip < 0)
+        info->pad = -spec_skip;
+      else if ((spec_skip & 0xff) != 0)
+        info->pad = spec_skip - 1;
+    }
   }
 }
 
