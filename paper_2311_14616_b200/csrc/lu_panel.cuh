@@ -474,8 +474,10 @@ __global__ void __launch_bounds__(NTX, 1)
   if constexpr (whole_spec_eligible<T, NB, RPT, NTX>())
   {
     // DevInfo::pad: panels still to skip (low byte) | back-off level (next
-    // byte): a beaten panel makes the next `level` panels not try (level 1, 2,
-    // 4, 8 on consecutive failures), a clean one resets it. Every CTA reads it
+    // byte): consecutive beaten panels make the next 0, 1, 3, 7 panels not try
+    // (level 1, 2, 4, 8), a clean one resets the level -- an isolated
+    // interchange (cfg 2a has one every ~7 panels) costs no skipped panel, a
+    // pivot-heavy matrix (cfg 4) tries one panel in eight. Every CTA reads it
     // before anyone writes it (kernel end).
     spec_skip = info->pad;
     if (spec_ok && (spec_skip & 0xff) == 0 && jb == NB)
@@ -487,7 +489,7 @@ __global__ void __launch_bounds__(NTX, 1)
         return;
       }
       const int level = min(max(2 * (spec_skip >> 8), 1), kSpecSkip);
-      spec_skip = -((level << 8) | level);  // beaten: negative = store at kernel end
+      spec_skip = -((level << 8) | (level - 1));  // beaten: negative = store at kernel end
     }
   }
   // Stage the panel rows in shared memory (coalesced columns, 8 columns of

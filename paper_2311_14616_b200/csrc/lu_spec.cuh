@@ -73,11 +73,7 @@ __device__ __forceinline__ SpecDiv spec_div_make(float piv)
 {
   SpecDiv d;
   d.piv = piv;
-#ifdef SPEC_X_APPROX_RCP
-  d.yh = __fdividef(1.0f, piv);
-#else
   d.yh = __frcp_rn(piv);
-#endif
   d.yl = __fmul_rn(__fmaf_rn(-piv, d.yh, 1.0f), d.yh);
   d.ok = exp_mid_f(piv);
   return d;
@@ -91,9 +87,6 @@ __device__ __forceinline__ SpecDiv spec_div_make(float piv)
 // divisions fail, i.e. about one 4096 x 64 panel in 200.
 __device__ __forceinline__ float spec_div(float a, const SpecDiv &d, bool act, bool &bad)
 {
-#ifdef SPEC_X_NOVERIFY
-  return __fmaf_rn(a, d.yh, __fmul_rn(a, d.yl));
-#else
   const float q = __fmaf_rn(a, d.yh, __fmul_rn(a, d.yl));
   const float v = __fmaf_rn(__fmaf_rn(-d.piv, q, a), d.yh, q);
   // an exactly zero numerator (structural zeros are common: the first and last
@@ -101,7 +94,6 @@ __device__ __forceinline__ float spec_div(float a, const SpecDiv &d, bool act, b
   const bool zero = a == 0.0f;
   bad |= act && !(d.ok && (zero || (v == q && exp_mid_f(a))));
   return zero ? __fmul_rn(a, d.piv) : q;
-#endif
 }
 
 template <int NB>
@@ -269,29 +261,23 @@ __device__ __forceinline__ void spec_diag_phase(float (&D)[2][NB / 8][8], SpecSh
 #pragma unroll
       for (int e = 0; e < 8; ++e)
         ub[e] = e >= kk ? __shfl_sync(0xffffffffu, D[PH][0][e], ol) : 0.0f;
-#ifndef SPEC_X_NOSTORE
       st8_if(own, Uk, D[PH][0]);
 #pragma unroll
       for (int j = 1; j < NBLK; ++j)
         if (j <= nlive)
           st8_if(own, Uk + 8 * j, D[PH][j]);
-#endif
       const float piv = ub[kk];
       const SpecDiv dv = spec_div_make(piv);
       const float pabs = fabsf(piv);
-#ifndef SPEC_X_NOCHECK
       if (piv == 0.0f)
         zj = min(zj, 8 * b + kk);
-#endif
       float l[2];
 #pragma unroll
       for (int sl = PH; sl < 2; ++sl)
       {
         const bool act = (sl == 1 && PH == 0) || lane > ol;
         const float v = act ? D[sl][0][kk] : 1.0f;
-#ifndef SPEC_X_NOCHECK
         beaten |= act && fabsf(v) > pabs;
-#endif
         l[sl] = spec_div(v, dv, act, beaten);
         D[sl][0][kk] = l[sl];
 #pragma unroll
@@ -299,7 +285,6 @@ __device__ __forceinline__ void spec_diag_phase(float (&D)[2][NB / 8][8], SpecSh
           D[sl][0][e] = upd(D[sl][0][e], l[sl], ub[e]);
       }
       __syncwarp();  // the owner's row is in shared memory
-#ifndef SPEC_X_NOLATER
 #pragma unroll
       for (int j = 1; j < NBLK; ++j)
         if (j <= nlive)
@@ -312,7 +297,6 @@ __device__ __forceinline__ void spec_diag_phase(float (&D)[2][NB / 8][8], SpecSh
             for (int e = 0; e < 8; ++e)
               D[sl][j][e] = upd(D[sl][j][e], l[sl], uj[e]);
         }
-#endif
     }
     // block b is final in every row still active: keep it (rank 0), rotate, publish progress
     if (stash)

@@ -142,7 +142,7 @@ int main()
       std::vector<float> got(A.size());
       cudaMemcpy(got.data(), dout, A.size() * 4, cudaMemcpyDeviceToHost);
       int bad = 0;
-      const int rows = mode == 0 ? 64 : m;
+      const int rows = (mode & 1) == 0 ? 64 : m;
       for (int i = 0; i < rows; ++i)
         for (int c = 0; c < NB; ++c)
           bad += memcmp(&got[(size_t)c * m + i], &ref[(size_t)c * m + i], 4) != 0;
