@@ -128,8 +128,10 @@ __device__ __forceinline__ void st8_if(bool pred, float *p, const float (&d)[8])
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t"
       "@p st.shared.v4.f32 [%1], {%2, %3, %4, %5};\n\t"
       "@p st.shared.v4.f32 [%1+16], {%6, %7, %8, %9};\n\t}\n" ::"r"((int)pred),
-      "r"(a), "f"(d[0]), "f"(d[1]), "f"(d[2]), "f"(d[3]), "f"(d[4]), "f"(d[5]), "f"(d[6]), "f"(d[7])
-      : "memory");
+      "r"(a), "f"(d[0]), "f"(d[1]), "f"(d[2]), "f"(d[3]), "f"(d[4]), "f"(d[5]), "f"(d[6]), "f"(d[7]));
+  // (no memory clobber: the step's __syncwarp orders these stores against the
+  // loads that read them; a clobber here would also pin every other load and
+  // store of the step in place)
 }
 __device__ __forceinline__ void st8(float *p, const float (&d)[8])
 {
@@ -251,16 +253,50 @@ __device__ __forceinline__ void spec_diag_phase(float (&D)[2][NB / 8][8], SpecSh
     const int b = 4 * PH + bb;
     const int nlive = NBLK - 1 - b;
     float *Uk0 = &sh.U[8 * b][8 * b];
+    // The later-block updates of step kk run one step late, between the
+    // shuffles of step kk+1 and its division: they are the bulk of the
+    // instructions and are not on the step-to-step dependency (current block
+    // of the next pivot row -> shuffle -> division -> in-block update), so
+    // they fill that chain's latency instead of adding to it. The owner of
+    // row kk+1 stores its later blocks right after they took update kk.
+    // (the pivot row's later blocks are loaded in one batch at the top of the
+    // step, before the shuffles: issued back to back they cost one
+    // shared-memory latency, loaded block by block in front of their FMAs they
+    // cost seven)
+    float lprev[2] = {0.0f, 0.0f};
+    float ujs[NBLK - 1][8];
+    auto later_load = [&](const float *Ukp) {
+#pragma unroll
+      for (int j = 1; j < NBLK; ++j)
+        if (j <= nlive)
+          ld8(ujs[j - 1], Ukp + 8 * j);
+    };
+    auto later_apply = [&]() {
+#pragma unroll
+      for (int j = 1; j < NBLK; ++j)
+        if (j <= nlive)
+        {
+#pragma unroll
+          for (int sl = PH; sl < 2; ++sl)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              D[sl][j][e] = upd(D[sl][j][e], lprev[sl], ujs[j - 1][e]);
+        }
+    };
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
     {
       const int ol = 8 * bb + kk;  // owner lane of pivot row 8b + kk
       float *Uk = Uk0 + kk * NB;
       const bool own = lane == ol;
+      if (kk > 0)
+        later_load(Uk - NB);  // step kk-1 (its row was stored one step ago)
       float ub[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e)
         ub[e] = e >= kk ? __shfl_sync(0xffffffffu, D[PH][0][e], ol) : 0.0f;
+      if (kk > 0)
+        later_apply();
       st8_if(own, Uk, D[PH][0]);
 #pragma unroll
       for (int j = 1; j < NBLK; ++j)
@@ -271,33 +307,23 @@ __device__ __forceinline__ void spec_diag_phase(float (&D)[2][NB / 8][8], SpecSh
       const float pabs = fabsf(piv);
       if (piv == 0.0f)
         zj = min(zj, 8 * b + kk);
-      float l[2];
 #pragma unroll
       for (int sl = PH; sl < 2; ++sl)
       {
         const bool act = (sl == 1 && PH == 0) || lane > ol;
         const float v = act ? D[sl][0][kk] : 1.0f;
         beaten |= act && fabsf(v) > pabs;
-        l[sl] = spec_div(v, dv, act, beaten);
-        D[sl][0][kk] = l[sl];
+        const float l = spec_div(v, dv, act, beaten);
+        lprev[sl] = l;
+        D[sl][0][kk] = l;
 #pragma unroll
         for (int e = kk + 1; e < 8; ++e)
-          D[sl][0][e] = upd(D[sl][0][e], l[sl], ub[e]);
+          D[sl][0][e] = upd(D[sl][0][e], l, ub[e]);
       }
       __syncwarp();  // the owner's row is in shared memory
-#pragma unroll
-      for (int j = 1; j < NBLK; ++j)
-        if (j <= nlive)
-        {
-          float uj[8];
-          ld8(uj, Uk + 8 * j);
-#pragma unroll
-          for (int sl = PH; sl < 2; ++sl)
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              D[sl][j][e] = upd(D[sl][j][e], l[sl], uj[e]);
-        }
     }
+    later_load(Uk0 + 7 * NB);  // the block's last step
+    later_apply();
     // block b is final in every row still active: keep it (rank 0), rotate, publish progress
     if (stash)
     {
