@@ -346,7 +346,17 @@ __device__ __forceinline__ bool whole_panel_spec(TG *__restrict__ A, int n, int 
     for (int b = 0; b < NBLK; ++b)
     {
       if (b > 0 && __any_sync(0xffffffffu, beaten))
+      {
+        // tell every CTA of the cluster, not only this one: the others would
+        // run their whole share before the verdict (plain remote stores; the
+        // verdict's cluster barrier completes them before any shared memory is reused)
         sh.abort = 1;
+        if (CS > 1 && lane < CS)
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(
+                           mapa(smem_addr(const_cast<const int *>(&sh.abort)), (uint32_t)lane)),
+                       "r"(1u)
+                       : "memory");
+      }
       while (sh.prog < 8 * (b + 1) && !sh.abort)
         __nanosleep(40);
       if (sh.abort)
