@@ -115,6 +115,48 @@ def test_lu_bitwise(orc, prec, kind, n, p, gpulib):
     assert same_bits(got, want)
 
 
+def _spec_case(kind, n):
+    """Matrices aimed at the whole-panel speculation of the binary32 panel kernel
+    (lu_spec.cuh): clean panels, uncertifiable quotients, isolated interchanges."""
+    rng = np.random.default_rng(123)
+    a = rng.uniform(-1.0, 1.0, (n, n))
+    if kind == "neg_diag_zeros":
+        # negative pivots and exact zeros of both signs: the zero-numerator rule
+        # (signed zero of the product) must match 0 / pivot
+        a[rng.random((n, n)) < 0.5] = 0.0
+        a[rng.random((n, n)) < 0.1] = -0.0
+        a[np.arange(n), np.arange(n)] = -(n * 1.0 + rng.uniform(0, 1, n))
+    elif kind == "late_interchange":
+        # diagonally dominant except single entries deep in a few panels
+        a[np.arange(n), np.arange(n)] = n * 1.0
+        for col, row in [(37, n - 3), (64 + 63, 64 + 64), (5 * 64 + 1, 5 * 64 + 2)]:
+            if row < n and col < n:
+                a[row, col] = 4.0 * n
+    elif kind == "tiny_entries":
+        # numerators below the certified range (|a| < 2^-60): the panel must fall
+        # back to the exchange algorithm's div.rn and still match
+        a[np.arange(n), np.arange(n)] = n * 1.0
+        a[rng.random((n, n)) < 0.05] *= 1e-30
+        a[np.arange(n), np.arange(n)] = n * 1.0
+    elif kind == "huge_pivots":
+        a[np.arange(n), np.arange(n)] = 1e25  # divisors above 2^61
+    return np.asfortranarray(a)
+
+
+@pytest.mark.parametrize("n", [300, 1000, 1500])
+@pytest.mark.parametrize("kind", ["neg_diag_zeros", "late_interchange", "tiny_entries", "huge_pivots"])
+def test_lu_speculation_edges(orc, kind, n, gpulib):
+    import torch
+    a = demote_host(_spec_case(kind, n), B32)
+    st, want, ipiv_want, _, _ = orc.lu(a, B32)
+    assert st == 0
+    d = to_dev(a)
+    ipiv = torch.zeros(n, dtype=torch.int32, device="cuda")
+    K().lu_factor(d, ipiv, n)
+    np.testing.assert_array_equal(ipiv.cpu().numpy(), ipiv_want)
+    assert same_bits(from_dev(d), want)
+
+
 @pytest.mark.parametrize("nb", [32, 64])
 def test_lu_bitwise_any_panel_width(orc, nb, gpulib):
     import torch
