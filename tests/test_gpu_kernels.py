@@ -237,6 +237,35 @@ def test_solve_mps_bitwise(orc, ts, tf, n, gpulib):
     assert same_bits(got, want)
 
 
+@pytest.mark.parametrize("ts,tf", [(B64, B32), (B32, B32), (B32, B16)])
+@pytest.mark.parametrize("kind", ["zeros", "tiny", "huge"])
+def test_solve_mps_uncertified_operands(orc, ts, tf, kind, gpulib):
+    """Right-hand sides whose back-substitution numerators fall outside the range
+    where the one-fma division can be certified (exact zeros of both signs,
+    magnitudes below 2^-60 / above 2^61): those slices take div.rn and the
+    result is still the reference's bit for bit."""
+    import torch
+    n = 777
+    a64 = greens(n, 800.0)
+    af = demote_host(a64, tf) if tf != B64 else a64
+    st, packed, ipiv, _, _ = orc.lu(af, tf)
+    rng = np.random.default_rng(9)
+    x64 = rng.uniform(-1.0, 1.0, n)
+    if kind == "zeros":
+        x64[rng.random(n) < 0.6] = 0.0
+        x64[rng.random(n) < 0.1] = -0.0
+        x64[n - 130:] = 0.0  # whole trailing blocks of zeros
+    elif kind == "tiny":
+        x64 *= 1e-25 if ts == B32 else 1e-160
+    else:
+        x64 *= 1e25 if ts == B32 else 1e160
+    x = x64.astype(NP[ts])
+    st, want = orc.solve_mps(ts, tf, packed, ipiv, x)
+    xd = to_dev(x)
+    K().solve_mps(to_dev(packed), torch.from_numpy(ipiv).cuda(), xd, tf=tf)
+    assert same_bits(from_dev(xd), want)
+
+
 @pytest.mark.parametrize("tw,tf", [(B64, B32), (B64, B16), (B32, B16)])
 @pytest.mark.parametrize("n", [2, 64, 333, 1024])
 def test_solve_lps_bitwise(orc, tw, tf, n, gpulib):
