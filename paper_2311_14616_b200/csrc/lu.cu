@@ -664,15 +664,29 @@ void configure_gemm()
   done.done();
 }
 
-// Speculative pivoting in the panel (lu_panel.cuh); MPIRG_PANEL_SPEC=0 turns
-// it off (every step then takes the cluster-wide exchange).
-static int panel_spec()
+// Speculative pivoting in the panel (lu_panel.cuh), a bit mask: 1 = per
+// eight-column block, 2 = whole panel first. MPIRG_PANEL_SPEC=0 turns both off
+// (every step then takes the cluster-wide exchange), MPIRG_PANEL_WHOLE=0 only
+// the whole-panel pass, MPIRG_PANEL_WHOLE_BATCH=0 only for batched launches
+// (measured on cfg 5b: 0.213 s with it, 0.227 s without -- the pass's shared
+// memory already limits the kernel to one CTA per SM either way).
+static int panel_spec(int ns)
 {
-  static const int v = [] {
+  static const int base = [] {
     const char *e = std::getenv("MPIRG_PANEL_SPEC");
     return e ? (std::atoi(e) != 0 ? 1 : 0) : 1;
   }();
-  return v;
+  static const int whole = [] {
+    const char *e = std::getenv("MPIRG_PANEL_WHOLE");
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : 1;
+  }();
+  static const int whole_batch = [] {
+    const char *e = std::getenv("MPIRG_PANEL_WHOLE_BATCH");
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : 1;
+  }();
+  if (!base)
+    return 0;
+  return 1 | ((ns > 1 ? whole_batch : whole) ? 2 : 0);
 }
 
 template <typename T, int NB, int RPT, int NTX = panel2::NT, typename TG = T>
@@ -693,7 +707,7 @@ void launch_panel_rpt(int cs, TG *a, int n, int k0, int jb, int *ipiv, int2 *mv,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT, NTX, TG>, a, n,
-                                      k0, jb, ipiv, mv, nm, info, panel_spec(), bs));
+                                      k0, jb, ipiv, mv, nm, info, panel_spec(ns), bs));
 }
 
 // Largest rows-per-thread the shared memory allows for (T, NB) at 256 threads.

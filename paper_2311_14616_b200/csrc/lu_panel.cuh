@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(NTX, 1)
     // pivot-heavy matrix (cfg 4) tries one panel in eight. Every CTA reads it
     // before anyone writes it (kernel end).
     spec_skip = info->pad;
-    if (spec_ok && (spec_skip & 0xff) == 0 && jb == NB)
+    if ((spec_ok & 2) && (spec_skip & 0xff) == 0 && jb == NB)
     {
       if (whole_panel_spec<NB, 2, NTX, TG>(A, n, k0, dsm, ipiv, info, CS, rank))
       {
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(NTX, 1)
     // (piv_rank is reset at the previous block's end / kernel start)
     // Arm the block exchange before this CTA sends any step message of the
     // block: a peer sends block data only after every CTA's last step message.
-    const bool try_spec = multi && spec_ok && skip == 0 && jb0 + IB <= jb;
+    const bool try_spec = multi && (spec_ok & 1) && skip == 0 && jb0 + IB <= jb;
     // (a speculative block arms it at block end, only if it is beaten)
     if (t == 0 && multi && bend < jb && !try_spec)
       mbar_expect_tx(&bars[2], (uint32_t)((bend - jb0) * rch * 16));
