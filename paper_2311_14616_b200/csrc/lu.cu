@@ -697,7 +697,10 @@ void launch_panel_rpt(int cs, TG *a, int n, int k0, int jb, int *ipiv, int2 *mv,
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, 1, ns);
   cfg.blockDim = dim3(NTX);
-  cfg.dynamicSmemBytes = panel2::panel_dyn_smem<T, NB, RPT, NTX>();
+  const int spec = panel_spec(ns);
+  // (the whole-panel pass needs more shared memory than the exchange algorithm)
+  cfg.dynamicSmemBytes = (spec & 2) ? panel2::panel_dyn_smem<T, NB, RPT, NTX>()
+                                    : panel2::panel_exact_smem<T, NB, RPT, NTX>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -707,7 +710,7 @@ void launch_panel_rpt(int cs, TG *a, int n, int k0, int jb, int *ipiv, int2 *mv,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT, NTX, TG>, a, n,
-                                      k0, jb, ipiv, mv, nm, info, panel_spec(ns), bs));
+                                      k0, jb, ipiv, mv, nm, info, spec, bs));
 }
 
 // Largest rows-per-thread the shared memory allows for (T, NB) at 256 threads.

@@ -208,10 +208,16 @@ __device__ __forceinline__ uint32_t cluster_size()
 // (the block's pivot rows: block columns from the step messages, right
 // columns from the block-end exchange).
 template <typename T, int NB, int RPT, int NTX = NT>
+__host__ __device__ constexpr size_t panel_exact_smem()
+{
+  return a16(sizeof(T) * (size_t)NB * RPT * NTX) + a16(sizeof(T) * (size_t)IB * NB);
+}
+// With the whole-panel speculation (which keeps its own layout in the same
+// buffer: lu_spec.cuh) enabled for the launch.
+template <typename T, int NB, int RPT, int NTX = NT>
 __host__ __device__ constexpr size_t panel_dyn_smem()
 {
-  const size_t exact = a16(sizeof(T) * (size_t)NB * RPT * NTX) + a16(sizeof(T) * (size_t)IB * NB);
-  // the whole-panel speculation (below) keeps its own layout in the same buffer
+  const size_t exact = panel_exact_smem<T, NB, RPT, NTX>();
   const size_t spec = (sizeof(T) == 4 && NB == 64 && RPT == 1 && NTX == 256)
                           ? a16(2 * sizeof(float) * (size_t)NB * NB + 256) + sizeof(float) * (size_t)2 * NB * NTX
                           : 0;
