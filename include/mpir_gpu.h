@@ -191,9 +191,11 @@ int mpirg_ir_solve(mpirg_factorization *f, const void *b, int b_on_device,
  * krylov_ir_solve_report: each correction is one left-preconditioned GMRES
  * solve (modified Gram-Schmidt, Givens rotations, at most `basissize` basis
  * vectors, relative tolerance 1e-2) with the low-precision factors as the
- * preconditioner, bitwise equal to the reference's. BiCGSTAB is not built
- * (MPIRG_ERR_INVALID_CONFIG). khist (inner iteration counts, one per
- * correction) and the breakdown flag of the last solve: _last_khist. */
+ * preconditioner; with BiCGSTAB one left-preconditioned bi-conjugate gradient
+ * stabilised solve (bicgstab_correction_into, 173-254: at most `basissize`
+ * iterations, relative tolerance 0.1). Both bitwise equal to the reference's.
+ * khist (inner iteration counts, one per correction) and the breakdown flag of
+ * the last solve: _last_khist. */
 enum mpirg_krylov_kind { MPIRG_KRYLOV_NONE = 0, MPIRG_KRYLOV_GMRES = 1, MPIRG_KRYLOV_BICGSTAB = 2 };
 int mpirg_factorization_enable_krylov(mpirg_factorization *f, int kind, int basissize,
                                       mpirg_error *err);

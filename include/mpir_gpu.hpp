@@ -511,8 +511,6 @@ public:
                    KrylovKind kind = KrylovKind::None, int basissize = 10, int device = -1)
     : cfg_((cfg.validate(), cfg))  // validated before any allocation (runtime.cpp:69)
   {
-    if (kind == KrylovKind::Bicgstab)
-      throw InvalidConfig("only GMRES corrections are built on the B200 path");
     if (kind != KrylovKind::None && basissize < 1)
       throw InvalidParameter("Krylov basis budget must be at least 1");
     if (cfg.tw == Precision::B16)

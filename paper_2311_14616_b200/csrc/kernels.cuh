@@ -265,7 +265,7 @@ struct GmresCtx
   const void *a_high = nullptr;
   const void *a_low = nullptr;
   const int *perm = nullptr;
-  void *basis = nullptr;    // (bs + 1) x n values of TW
+  void *basis = nullptr;    // max(bs + 1, 7) x n values of TW
   void *tmp = nullptr;      // n values of TW
   void *dots = nullptr;     // bs + 2 device scalars of TW
   void *h_dots = nullptr;   // pinned mirror
@@ -278,6 +278,9 @@ struct GmresCtx
 // w (n values of TW on the device): the residual on entry, the correction on
 // exit (d may alias r, krylov_ir.hpp:57). Synchronises the stream.
 void gmres_correction(GmresCtx &c, void *w, int *iters, bool *breakdown);
+// bicgstab_correction_into (krylov_ir.hpp:173-254): same context (bs = the
+// iteration budget, rtol = 0.1, seven work vectors at the start of basis).
+void bicgstab_correction(GmresCtx &c, void *w, int *iters, bool *breakdown);
 void launch_demote_vec(int tw, int tr, int n, const void *r, void *w, cudaStream_t s);
 void launch_ir_update(int tw, int tr, int n, const void *w, void *x, unsigned long long *dnorm,
                       unsigned long long *xnorm, cudaStream_t s);

@@ -317,6 +317,173 @@ void gmres_t(GmresCtx &c, void *w_inout, int *iters, bool *breakdown)
   *iters = k;
   *breakdown = brk;
 }
+// out_i = fma(sc, b_i, a_i) (out may alias a): the reference build fuses every
+// "x +- scalar * y" of the BiCGSTAB vector updates into one FMA.
+template <typename T>
+__global__ void vfma_kernel(T *__restrict__ out, const T *a, const T *__restrict__ b, T sc, int n)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = kfma(sc, b[i], a[i]);
+}
+// p_i = fma(beta, fma(-omega, v_i, p_i), rr_i) (krylov_ir.hpp:248-249)
+template <typename T>
+__global__ void bicg_p_kernel(T *__restrict__ p, const T *__restrict__ rr, const T *__restrict__ v,
+                              T beta, T omega, int n)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = kfma(beta, kfma(-omega, v[i], p[i]), rr[i]);
+}
+
+// bicgstab_correction_into (krylov_ir.hpp:173-254) as the reference build runs
+// it: left-preconditioned BiCGSTAB on M^-1 A d = M^-1 r from d = 0, at most
+// `bs` iterations, rtol 0.1. The dot products follow the same fold-left rule as
+// the GMRES ones (dot: half-vector epilogue; the a == b instances -- nrm2 and
+// t.t -- as nrm2 does); every vector update is one FMA per element; the five
+// scalars per iteration (alpha, omega, beta from two quotients and a product)
+// are computed on the host in the working precision. Workspace: seven vectors
+// at the start of c.basis. Four host synchronisations per iteration.
+template <typename T>
+void bicgstab_t(GmresCtx &c, void *w_inout, int *iters, bool *breakdown)
+{
+  const int n = c.n;
+  cudaStream_t s = c.s;
+  T *w = static_cast<T *>(w_inout);
+  T *z = static_cast<T *>(c.basis);
+  T *rr = z + (size_t)n, *rhat = z + 2 * (size_t)n, *p = z + 3 * (size_t)n, *v = z + 4 * (size_t)n,
+    *sv = z + 5 * (size_t)n, *tv = z + 6 * (size_t)n;
+  T *tmp = static_cast<T *>(c.tmp);
+  T *dots = static_cast<T *>(c.dots);
+  T *hd = static_cast<T *>(c.h_dots);
+  auto precond = [&](const T *src, T *dst) {
+    TrsvArgs a{};
+    a.ts = c.tw;
+    a.tf = c.tf;
+    a.tin = c.tw;
+    a.lps = 0;
+    a.ir = 0;
+    a.n = n;
+    a.lu = c.a_low;
+    a.perm = c.perm;
+    a.rin = src;
+    a.y = c.y;
+    a.out = dst;
+    a.info = c.info;
+    launch_trsv(a, *c.tws, s);
+  };
+  auto dot = [&](const T *a, const T *b, int slot, bool half_step = true) {
+    dot_seq_kernel<T><<<1, 256, 0, s>>>(a, b, n, reduction_unfused(n, (int)sizeof(T), half_step),
+                                        dots + slot);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  };
+  constexpr bool nrm_half = sizeof(T) == 4;
+  auto fetch = [&](int count) {
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(hd, dots, sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+    MPIRG_CUDA_CHECK(
+        cudaMemcpyAsync(c.h_info, c.info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
+    MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+    return c.h_info->nonfinite == 0;
+  };
+  auto matvec = [&](const T *x, T *y) {
+    matvec_kernel<T><<<(n + 31) / 32, 32, 0, s>>>(static_cast<const T *>(c.a_high), n, x, y);
+    MPIRG_CUDA_CHECK(cudaGetLastError());
+  };
+  const int g = grid_for(n);
+  *iters = 0;
+  *breakdown = false;
+  c.nonfinite = false;
+  precond(w, z);
+  dot(z, z, 0, nrm_half);
+  if (!fetch(1))
+  {
+    c.nonfinite = true;
+    return;
+  }
+  MPIRG_CUDA_CHECK(cudaMemsetAsync(w, 0, sizeof(T) * n, s));  // d = 0
+  const double znorm = static_cast<double>(host_sqrt<T>(hd[0]));
+  if (znorm == 0.0)
+    return;
+  const double target = c.rtol * znorm;
+  for (T *dst : {rr, rhat, p})
+    MPIRG_CUDA_CHECK(cudaMemcpyAsync(dst, z, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  dot(rhat, rr, 0);
+  if (!fetch(1))
+  {
+    c.nonfinite = true;
+    return;
+  }
+  T rho = hd[0];
+  int it = 0;
+  bool brk = false;
+  while (it < c.bs)
+  {
+    matvec(p, tmp);
+    precond(tmp, v);
+    dot(rhat, v, 0);
+    if (!fetch(1))
+    {
+      c.nonfinite = true;
+      return;
+    }
+    const T denom = hd[0];
+    if (denom == T(0))
+    {
+      brk = true;
+      break;
+    }
+    const T alpha = rho / denom;
+    vfma_kernel<T><<<g, 256, 0, s>>>(sv, rr, v, -alpha, n);
+    vfma_kernel<T><<<g, 256, 0, s>>>(w, w, p, alpha, n);
+    ++it;
+    dot(sv, sv, 0, nrm_half);
+    if (!fetch(1))
+    {
+      c.nonfinite = true;
+      return;
+    }
+    if (static_cast<double>(host_sqrt<T>(hd[0])) <= target)
+      break;
+    matvec(sv, tmp);
+    precond(tmp, tv);
+    dot(tv, tv, 0, nrm_half);
+    dot(tv, sv, 1);
+    if (!fetch(2))
+    {
+      c.nonfinite = true;
+      return;
+    }
+    const T tt = hd[0];
+    if (tt == T(0))
+    {
+      brk = true;
+      break;
+    }
+    const T omega = hd[1] / tt;
+    vfma_kernel<T><<<g, 256, 0, s>>>(w, w, sv, omega, n);
+    vfma_kernel<T><<<g, 256, 0, s>>>(rr, sv, tv, -omega, n);
+    dot(rr, rr, 0, nrm_half);
+    dot(rhat, rr, 1);
+    if (!fetch(2))
+    {
+      c.nonfinite = true;
+      return;
+    }
+    if (static_cast<double>(host_sqrt<T>(hd[0])) <= target)
+      break;
+    const T rho_new = hd[1];
+    if (rho_new == T(0) || omega == T(0))
+    {
+      brk = true;
+      break;
+    }
+    const T beta = (rho_new / rho) * (alpha / omega);
+    bicg_p_kernel<T><<<g, 256, 0, s>>>(p, rr, v, beta, omega, n);
+    rho = rho_new;
+  }
+  MPIRG_CUDA_CHECK(cudaGetLastError());
+  MPIRG_CUDA_CHECK(cudaStreamSynchronize(s));
+  *iters = it;
+  *breakdown = brk;
+}
 }  // namespace
 
 void gmres_correction(GmresCtx &c, void *w, int *iters, bool *breakdown)
@@ -325,6 +492,14 @@ void gmres_correction(GmresCtx &c, void *w, int *iters, bool *breakdown)
     gmres_t<double>(c, w, iters, breakdown);
   else
     gmres_t<float>(c, w, iters, breakdown);
+}
+
+void bicgstab_correction(GmresCtx &c, void *w, int *iters, bool *breakdown)
+{
+  if (c.tw == B64)
+    bicgstab_t<double>(c, w, iters, breakdown);
+  else
+    bicgstab_t<float>(c, w, iters, breakdown);
 }
 
 void launch_demote_vec(int tw, int tr, int n, const void *r, void *w, cudaStream_t s)

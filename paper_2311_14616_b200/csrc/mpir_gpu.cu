@@ -213,7 +213,8 @@ struct mpirg_factorization
     free_krylov();
     kry_kind = kind;
     kry_bs = basissize;
-    kry_basis = dalloc_bytes((size_t)(basissize + 1) * n * tw_bytes());
+    // GMRES: basissize + 1 basis vectors; BiCGSTAB: its seven work vectors
+    kry_basis = dalloc_bytes((size_t)std::max(basissize + 1, 7) * n * tw_bytes());
     kry_tmp = dalloc_bytes((size_t)n * tw_bytes());
     kry_w = dalloc_bytes((size_t)n * tw_bytes());
     kry_dots = dalloc_bytes((size_t)(basissize + 2) * 8);
@@ -620,7 +621,13 @@ struct mpirg_factorization
         g.s = s;
         int its = 0;
         bool brk = false;
-        gmres_correction(g, kry_w, &its, &brk);
+        if (kry_kind == MPIRG_KRYLOV_BICGSTAB)
+        {
+          g.rtol = 0.1;  // bicgstab_correction_into's default
+          bicgstab_correction(g, kry_w, &its, &brk);
+        }
+        else
+          gmres_correction(g, kry_w, &its, &brk);
         if (g.nonfinite)
         {
           if (it == 0)
@@ -2209,9 +2216,8 @@ int mpirg_factorization_enable_krylov(mpirg_factorization *f, int kind, int basi
     }
     if (basissize < 1)
       throw ApiError{MPIRG_ERR_INVALID_PARAM, "Krylov basis budget must be at least 1"};
-    if (kind != MPIRG_KRYLOV_GMRES)
-      throw ApiError{MPIRG_ERR_INVALID_CONFIG,
-                     "only GMRES corrections are built on the B200 path"};
+    if (kind != MPIRG_KRYLOV_GMRES && kind != MPIRG_KRYLOV_BICGSTAB)
+      throw ApiError{MPIRG_ERR_INVALID_PARAM, "unknown Krylov kind"};
     f->enable_krylov(kind, basissize);
   });
 }

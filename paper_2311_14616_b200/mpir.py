@@ -11,11 +11,11 @@ import. Everything numeric runs on the GPU through libmpir_gpu.so:
 * ``Factorization.solve`` -> ir_solve_report (ir_engine.hpp:291-297).
 * ``solve`` -> factor once and refine (bindings.cpp:221-240).
 
-``krylov="gmres"`` attaches the reference's GMRES workspace: ``solve`` is then
-krylov_ir_solve_report (krylov_ir.hpp:297-318) with GMRES corrections on the
-device, bitwise equal to the reference, and the report carries ``khist``.
-BiCGSTAB corrections and ``direct_solve`` are not built (SURVEY.md section
-8(f)); they raise instead of silently running on the CPU.
+``krylov="gmres"`` / ``krylov="bicgstab"`` attach the reference's Krylov
+workspace: ``solve`` is then krylov_ir_solve_report (krylov_ir.hpp:297-318)
+with GMRES / BiCGSTAB corrections on the device, bitwise equal to the
+reference, and the report carries ``khist``. ``direct_solve`` is not built
+(SURVEY.md section 8(f)); it raises instead of silently running on the CPU.
 """
 from __future__ import annotations
 
@@ -128,8 +128,6 @@ class Factorization:
             krylov if krylov is None else str(krylov).lower(), -1)
         if kind < 0:
             raise InvalidParameter("unknown Krylov kind (gmres, bicgstab or none)")
-        if kind == 2:
-            raise InvalidConfig("only GMRES corrections are built on the B200 path")
         if kind and int(basissize) < 1:
             raise InvalidParameter("Krylov basis budget must be at least 1")
         cfg = resolve_config(parse_precision(working),

@@ -1,4 +1,4 @@
-"""GMRES-IR on the device (krylov_ir.hpp:62-171, 297-318)
+"""GMRES-IR and BiCGSTAB-IR on the device (krylov_ir.hpp:62-254, 297-318)
 against the compiled reference's krylov_ir_solve_report on the same inputs:
 solution bits, residual / correction histories, inner iteration counts and the
 stopping reason must all be equal.
@@ -36,7 +36,8 @@ def _problem(kind, n):
     (0, 2, 0, "randn", 512, 3),     # budget exhausted before the tolerance
     (0, 0, 0, "randn", 300, 5),
 ])
-def test_gmres_ir_bitwise_vs_compiled_reference(gpulib, ref, tw, tf, tr, kind, n, bs):
+@pytest.mark.parametrize("solver", ["gmres", "bicgstab"])
+def test_krylov_ir_bitwise_vs_compiled_reference(gpulib, ref, solver, tw, tf, tr, kind, n, bs):
     from paper_2311_14616_b200 import mpir
     if not hasattr(ref, "_krylov_ir"):
         pytest.skip("compiled reference built without the Krylov driver")
@@ -45,11 +46,11 @@ def test_gmres_ir_bitwise_vs_compiled_reference(gpulib, ref, tw, tf, tr, kind, n
         a = a.astype(np.float32).astype(np.float64)
         b = b.astype(np.float32).astype(np.float64)
     want = ref.krylov_ir(tw, tf, tr, a.astype(np.float32) if tw == 1 else a,
-                         b.astype(np.float32) if tw == 1 else b, basissize=bs, resid_term=False,
-                         ce=10.0, litmax=12)
+                         b.astype(np.float32) if tw == 1 else b, kind=solver, basissize=bs,
+                         resid_term=False, ce=10.0, litmax=12)
     assert want["status"] == "ok"
     f = mpir.Factorization(a, working=NAMES[tw], factor=NAMES[tf], residual=NAMES[tr],
-                           resid_term=False, krylov="gmres", basissize=bs)
+                           resid_term=False, krylov=solver, basissize=bs)
     got = f.solve(b, ce=10.0, litmax=12)
     assert got["khist"] == [int(k) for k in want["khist"]]
     assert got["reason"] == want["reason"]
@@ -82,5 +83,7 @@ def test_krylov_argument_validation(gpulib):
     a = greens(64, 1.0)
     with pytest.raises(mpir.InvalidParameter):
         mpir.Factorization(a, krylov="gmres", basissize=0)
-    with pytest.raises(mpir.InvalidConfig):
-        mpir.Factorization(a, krylov="bicgstab")
+    with pytest.raises(mpir.InvalidParameter):
+        mpir.Factorization(a, krylov="bicgstab", basissize=0)
+    with pytest.raises(mpir.InvalidParameter):
+        mpir.Factorization(a, krylov="cg")
