@@ -258,6 +258,18 @@ class Factorization:
                 "breakdown": breakdown,
                 "reason": L.REASONS[rep.reason], "seconds": sec, "device_ms": rep.solve_ms}
 
+    def solve_many(self, bs, **kw) -> list:
+        """Several right-hand sides against the one factorization: the columns of a
+        2-D ``bs`` (or an iterable of vectors), one ir_solve_report each on the
+        handle's reused buffers -- each report equals the single ``solve`` of its
+        column bit for bit. (The reference has no multi-right-hand-side entry
+        point: bindings.cpp:38 takes a 1-D b; its users loop exactly like this,
+        test_mp_structures.cpp:141-196.)"""
+        arr = np.asarray(bs, dtype=np.float64) if not isinstance(bs, (list, tuple)) else None
+        cols = ([arr[:, j] for j in range(arr.shape[1])] if arr is not None and arr.ndim == 2
+                else [arr] if arr is not None else list(bs))
+        return [self.solve(np.ascontiguousarray(c), **kw) for c in cols]
+
     def refactor(self, a) -> None:
         """Refactor a new matrix of the same size in place (runtime.cpp:122-134)."""
         acm = _colmajor(a)

@@ -169,3 +169,20 @@ def test_singular_matrix(gpulib):
     with pytest.raises(m.SingularPivot) as ei:
         m.Factorization(s, factor="single")
     assert ei.value.column == 2
+
+
+def test_solve_many_equals_single_solves(gpulib):
+    """Several right-hand sides on one handle: each report is the single solve's, bit for bit."""
+    from paper_2311_14616_b200 import mpir
+    n = 300
+    a = greens(n, 800.0)
+    rng = np.random.default_rng(4)
+    bs = rng.standard_normal((n, 3))
+    f = mpir.Factorization(a, working="double", factor="single", resid_term=False)
+    many = f.solve_many(bs, ce=10.0, litmax=20)
+    assert len(many) == 3
+    for j, rep in enumerate(many):
+        one = mpir.Factorization(a, working="double", factor="single", resid_term=False).solve(
+            bs[:, j].copy(), ce=10.0, litmax=20)
+        assert rep["reason"] == one["reason"] and rep["rhist"] == one["rhist"]
+        assert np.array_equal(rep["x"].view(np.uint64), one["x"].view(np.uint64))
