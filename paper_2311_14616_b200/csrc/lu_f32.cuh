@@ -33,7 +33,11 @@ constexpr int MT_COLS = 32;  // columns per CTA of the U12 solve (4 warps x 8)
 // ut[(ut_row + kk) * n + col] (row-major, contiguous along columns) so the
 // trailing update can stage it with TMA. The L factors are read from Ls (the
 // matrix itself, or the snapshot of the panel taken for late columns).
-template <int NB, bool PEND>
+// CPW columns per warp (4 CPW per CTA): 8 for throughput (the bulk of the
+// columns), 2 for the critical chain's next-panel block, whose 2 x NB
+// sequential steps (shuffle + FMA each) then cost their latency instead of
+// the issue time of eight interleaved columns.
+template <int NB, bool PEND, int CPW = 8>
 __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, int k0, int jb,
                                                   int cb, int ce,
                                                   const int2 *__restrict__ moves,
@@ -55,13 +59,14 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
   const size_t utp = ut_ld ? (size_t)ut_ld : (size_t)n;
   __shared__ float Lp[PEND ? NB : 1][NB + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int col0 = cb + blockIdx.x * MT_COLS + warp * 8;
+  constexpr int MTC = 4 * CPW;  // columns per CTA
+  const int col0 = cb + blockIdx.x * MTC + warp * CPW;
   // Every load that does not depend on the row moves is issued up front (the
   // L factors, the move count, this warp's panel rows and, for PEND, step
   // kp's U rows): on the LU's critical chain each dependent round trip costs
   // about a microsecond. The panel rows are reloaded if rows moved.
-  float x[8][RL];
-  float uv[8][PEND ? RL : 1];
+  float x[CPW][RL];
+  float uv[CPW][PEND ? RL : 1];
   int nm;
   {
     constexpr int PT = (NB * NB + 127) / 128;
@@ -77,7 +82,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
     }
     nm = *nmoves;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < CPW; ++u)
 #pragma unroll
       for (int h = 0; h < RL; ++h)
       {
@@ -108,9 +113,9 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
       const int e = lane + 32 * q;
       mv[q] = e < nm ? moves[e] : make_int2(-1, -1);
     }
-    float v[8][PER];
+    float v[CPW][PER];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < CPW; ++u)
       if (col0 + u < ce)
       {
         const float *cp = A + (size_t)(col0 + u) * n;
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
       }
     __syncwarp();
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < CPW; ++u)
       if (col0 + u < ce)
       {
         float *cp = A + (size_t)(col0 + u) * n;
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
     __syncwarp();
     // the panel rows after the moves (this warp's columns only)
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < CPW; ++u)
 #pragma unroll
       for (int h = 0; h < RL; ++h)
       {
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
       for (int h = 0; h < RL; ++h)
         lv[h] = Lp[lane + 32 * h][kk];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < CPW; ++u)
       {
         float src = uv[u][0];
 #pragma unroll
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
       lv[h] = (i > kk && i < jb) ? L[i][kk] : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < CPW; ++u)
     {
       float src = x[u][0];
 #pragma unroll
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
     }
   }
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < CPW; ++u)
 #pragma unroll
     for (int h = 0; h < RL; ++h)
     {
@@ -209,15 +214,15 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
   // transposed copy through shared memory: 128-byte row segments of ut
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < CPW; ++u)
 #pragma unroll
     for (int h = 0; h < RL; ++h)
-      L[lane + 32 * h][warp * 8 + u] = x[u][h];
+      L[lane + 32 * h][warp * CPW + u] = x[u][h];
   __syncthreads();
-  const int cbase = cb + blockIdx.x * MT_COLS;
-  for (int idx = threadIdx.x; idx < jb * MT_COLS; idx += 128)
+  const int cbase = cb + blockIdx.x * MTC;
+  for (int idx = threadIdx.x; idx < jb * MTC; idx += 128)
   {
-    const int kk = idx / MT_COLS, c = idx % MT_COLS;
+    const int kk = idx / MTC, c = idx % MTC;
     if (cbase + c < ce)
       ut[(size_t)(ut_row + kk) * utp + cbase + c] = L[kk][c];
   }
