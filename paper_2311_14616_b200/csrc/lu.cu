@@ -1396,13 +1396,13 @@ static void f32_mt(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 
   if (ce - cb <= NB)
   {
     // the critical chain's next-panel block: two columns per warp
-    constexpr int MTC = 8;
+    constexpr int MTC = 4;
     const int g = (ce - cb + MTC - 1) / MTC;
     if (kp >= 0)
-      f32u::mt2_kernel<NB, true, 2><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, kp, P.ut,
+      f32u::mt2_kernel<NB, true, 1><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, kp, P.ut,
                                                      ut_row, P.ls);
     else
-      f32u::mt2_kernel<NB, false, 2><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, 0, P.ut,
+      f32u::mt2_kernel<NB, false, 1><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, 0, P.ut,
                                                       ut_row, P.ls);
   }
   else

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
       }
     }
   }
-#pragma unroll 1
+#pragma unroll 4
   for (int kk = 0; kk < jb; ++kk)
   {
     const int hk = kk >> 5, lk = kk & 31;
