@@ -1356,6 +1356,10 @@ struct F32Plan
   float *a = nullptr, *ut = nullptr;
   const float *ls = nullptr;  // where the L factors are read (a, or the panel snapshots)
   int n = 0;
+  // columns per warp of the critical next-panel U12 solve: 1 from device memory
+  // (LU 4.01 -> 3.81 ms on cfg 2a), 2 inside the streamed refactor, whose late
+  // chunks run beside the chain (there 1 measured slower: 4.85 vs 4.64 ms)
+  int next_cpw = 2;
 };
 
 static void f32_encode(CUtensorMap *map, float *base, int inner, int outer, int box0)
@@ -1393,16 +1397,26 @@ static void f32_mt(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 
   if (ce <= cb)
     return;
   prof_begin(KC_TRSM, s);
-  if (ce - cb <= NB)
+  if (ce - cb <= NB && P.next_cpw == 1)
   {
-    // the critical chain's next-panel block: two columns per warp
-    constexpr int MTC = 4;
-    const int g = (ce - cb + MTC - 1) / MTC;
+    // the critical chain's next-panel block: one column per warp
+    const int g = (ce - cb + 3) / 4;
     if (kp >= 0)
       f32u::mt2_kernel<NB, true, 1><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, kp, P.ut,
                                                      ut_row, P.ls);
     else
       f32u::mt2_kernel<NB, false, 1><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, 0, P.ut,
+                                                      ut_row, P.ls);
+  }
+  else if (ce - cb <= NB)
+  {
+    // the same block with two columns per warp
+    const int g = (ce - cb + 7) / 8;
+    if (kp >= 0)
+      f32u::mt2_kernel<NB, true, 2><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, kp, P.ut,
+                                                     ut_row, P.ls);
+    else
+      f32u::mt2_kernel<NB, false, 2><<<g, 128, 0, s>>>(P.a, P.n, k0, jb, cb, ce, mv, nm, 0, P.ut,
                                                       ut_row, P.ls);
   }
   else
@@ -1656,6 +1670,13 @@ void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, Dev
   const int np = ws.npanels;
   F32Plan P;
   f32_plan_make(P, a, n, static_cast<float *>(ws.ut), 2 * NB);
+  {
+    static const int forced = [] {
+      const char *e = std::getenv("MPIRG_NEXT_CPW");
+      return e ? std::atoi(e) : 0;
+    }();
+    P.next_cpw = forced ? forced : (late ? 2 : 1);
+  }
   // late columns: chunk c (c >= 1) is updated on its own stream from panel
   // snapshots until step join[c]; the regular schedule's far columns end at
   // rlim(p) = the first column of the first chunk not yet joined
