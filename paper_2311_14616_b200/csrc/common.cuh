@@ -248,6 +248,20 @@ struct DevInfo
   int pad;
 };
 
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may become resident while
+// its predecessor in the stream still runs; pdl_wait() holds it until the
+// predecessor has completed and its writes are visible (no-op for a plain
+// launch), pdl_trigger() lets the successor become resident early.
+__device__ __forceinline__ void pdl_wait()
+{
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger()
+{
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
 }  // namespace mpirg
 
 #define MPIRG_CUDA_CHECK(expr)                                                        \

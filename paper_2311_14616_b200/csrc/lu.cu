@@ -670,6 +670,17 @@ void configure_gemm()
 // the whole-panel pass, MPIRG_PANEL_WHOLE_BATCH=0 only for batched launches
 // (measured on cfg 5b: 0.213 s with it, 0.227 s without -- the pass's shared
 // memory already limits the kernel to one CTA per SM either way).
+// MPIRG_LU_PDL=1: programmatic dependent launch along the binary32 LU's chain
+// (U12 solve -> update -> next panel); same kernels, same results.
+static bool lu_pdl()
+{
+  static const bool v = [] {
+    const char *e = std::getenv("MPIRG_LU_PDL");
+    return e && std::atoi(e) != 0 && !tool_attached();
+  }();
+  return v;
+}
+
 static int panel_spec(int ns)
 {
   static const int base = [] {
@@ -702,13 +713,19 @@ void launch_panel_rpt(int cs, TG *a, int n, int k0, int jb, int *ipiv, int2 *mv,
   cfg.dynamicSmemBytes = (spec & 2) ? panel2::panel_dyn_smem<T, NB, RPT, NTX>()
                                     : panel2::panel_exact_smem<T, NB, RPT, NTX>();
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (lu_pdl() && ns == 1)
+  {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel2::lu_panel2_kernel<T, NB, RPT, NTX, TG>, a, n,
                                       k0, jb, ipiv, mv, nm, info, spec, bs));
 }
@@ -1392,12 +1409,28 @@ static void f32_plan_make(F32Plan &p, float *a, int n, float *ut, int ut_rows,
 
 template <int NB>
 static void f32_mt(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 *mv,
-                   const int *nm, int kp, int ut_row, cudaStream_t s)
+                   const int *nm, int kp, int ut_row, cudaStream_t s, bool chain = false)
 {
   if (ce <= cb)
     return;
   prof_begin(KC_TRSM, s);
-  if (ce - cb <= NB && P.next_cpw == 1)
+  if (ce - cb <= NB && P.next_cpw == 1 && chain && kp < 0 && lu_pdl())
+  {
+    // right behind the panel in the chain's stream: programmatic launch
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((ce - cb + 3) / 4);
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, f32u::mt2_kernel<NB, false, 1>, P.a, P.n, k0, jb, cb,
+                                        ce, mv, nm, 0, P.ut, ut_row, (const float *)P.ls,
+                                        BatchStride{}, 0));
+  }
+  else if (ce - cb <= NB && P.next_cpw == 1)
   {
     // the critical chain's next-panel block: one column per warp
     const int g = (ce - cb + 3) / 4;
@@ -1503,6 +1536,23 @@ static void f32_gemm_t(const CUtensorMap &ma, const CUtensorMap &mu, const F32Pl
   }
   const int c0 = k0 + K;
   const dim3 grid((P.n - c0 + BM - 1) / BM, (ce - cb + BM - 1) / BM);
+  if (BM == 64 && lu_pdl() && ce - cb <= 64)
+  {
+    // the chain's update right behind its U12 solve in the same stream
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = f32u::gemm_tma_smem<BM>();
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MPIRG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, f32u::gemm_tma_kernel<BM>, ma, mu, P.a, P.n, k0, K,
+                                        ut_row, cb, ce));
+    return;
+  }
   f32u::gemm_tma_kernel<BM><<<grid, 256, f32u::gemm_tma_smem<BM>(), s>>>(ma, mu, P.a, P.n, k0,
                                                                         K, ut_row, cb, ce);
   MPIRG_CUDA_CHECK(cudaGetLastError());
@@ -1738,7 +1788,7 @@ void lu_run_f32_body(float *a, int n, int *ipiv, int *perm, LuWorkspace &ws, Dev
         tl.mark(p, 2, s);
       else
       {
-        f32_mt<NB>(P, k0, jb, c0, cnext, mv, nm, -1, ur, s);
+        f32_mt<NB>(P, k0, jb, c0, cnext, mv, nm, -1, ur, s, true);
         tl.mark(p, 2, s);
         f32_gemm(P, k0, jb, ur, c0, cnext, s);
       }

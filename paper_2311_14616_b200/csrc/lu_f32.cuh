@@ -49,6 +49,9 @@ __global__ void __launch_bounds__(128) mt2_kernel(float *__restrict__ A, int n, 
   constexpr int PER = (2 * NB + 31) / 32;
   constexpr int RL = (NB + 31) / 32;  // panel rows per lane
   __shared__ float L[NB][NB + 1];
+  if constexpr (CPW < 8)
+    pdl_trigger();  // the chain's update may become resident while this solve runs
+  pdl_wait();
   // batched launches (config 5b): system blockIdx.z; its U12 copy occupies
   // columns [z n, z n + n) of a ut with row pitch ut_ld = n * (systems)
   A += (size_t)blockIdx.z * bs.a;
@@ -252,6 +255,9 @@ __global__ void __launch_bounds__(256, BM == 128 ? 2 : 3)
   constexpr uint32_t CHUNK = BM * GKC * sizeof(float);
   extern __shared__ unsigned char gsm_raw[];
   __shared__ __align__(8) uint64_t full[GST];
+  pdl_wait();
+  if constexpr (BM == 64)
+    pdl_trigger();
   float *base = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(gsm_raw) + 127) &
                                           ~uintptr_t(127));
   float *As = base;                   // [GST][GKC][BM]

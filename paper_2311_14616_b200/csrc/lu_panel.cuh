@@ -443,6 +443,8 @@ __global__ void __launch_bounds__(NTX, 1)
                      int spec_ok, BatchStride bs)
 {
   constexpr int NT = NTX;  // hides the namespace default inside this kernel
+  pdl_trigger();
+  pdl_wait();
   A += (size_t)blockIdx.z * bs.a;
   ipiv += (size_t)blockIdx.z * bs.vec;
   moves += (size_t)blockIdx.z * bs.moves;
