@@ -670,13 +670,14 @@ void configure_gemm()
 // the whole-panel pass, MPIRG_PANEL_WHOLE_BATCH=0 only for batched launches
 // (measured on cfg 5b: 0.213 s with it, 0.227 s without -- the pass's shared
 // memory already limits the kernel to one CTA per SM either way).
-// MPIRG_LU_PDL=1: programmatic dependent launch along the binary32 LU's chain
-// (U12 solve -> update -> next panel); same kernels, same results.
-static bool lu_pdl()
+// Programmatic dependent launch along the binary32 LU's chain: level 1 (default)
+// U12 solve -> update -> next panel, level 2 also panel -> U12 solve (no gain
+// measured), MPIRG_LU_PDL=0 plain launches; same kernels, same results.
+static int lu_pdl()
 {
-  static const bool v = [] {
+  static const int v = [] {
     const char *e = std::getenv("MPIRG_LU_PDL");
-    return e && std::atoi(e) != 0 && !tool_attached();
+    return tool_attached() ? 0 : (e ? std::atoi(e) : 1);
   }();
   return v;
 }
@@ -1414,7 +1415,7 @@ static void f32_mt(const F32Plan &P, int k0, int jb, int cb, int ce, const int2 
   if (ce <= cb)
     return;
   prof_begin(KC_TRSM, s);
-  if (ce - cb <= NB && P.next_cpw == 1 && chain && kp < 0 && lu_pdl())
+  if (ce - cb <= NB && P.next_cpw == 1 && chain && kp < 0 && lu_pdl() >= 2)
   {
     // right behind the panel in the chain's stream: programmatic launch
     cudaLaunchConfig_t cfg = {};

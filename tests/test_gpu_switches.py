@@ -45,7 +45,8 @@ SWITCHES = [
     {"MPIRG_LU_GREEN": "0"},
     {"MPIRG_LU_GRAPH": "0"},
     {"MPIRG_GEMM": "scalar"},
-    {"MPIRG_LU_PDL": "1"},
+    {"MPIRG_LU_PDL": "0"},
+    {"MPIRG_LU_PDL": "2"},
 ]
 
 
